@@ -1,0 +1,1102 @@
+// C ABI of libqsocp_cuda.so (include/qsocp_cuda.h): handle, setup, the
+// per-kernel entry points and the device-resident IPM phases.
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qsocp_cuda.h"
+#include "cone_kernels.h"
+#include "host_setup.h"
+#include "kkt_kernels.h"
+#include "ldl.h"
+#include "spmv_kernels.h"
+
+namespace {
+
+thread_local std::string g_error;
+
+enum TimerCat { T_CONE = 0, T_KKT, T_RESID, T_FACTOR, T_SOLVE, T_REFINE, T_ANALYSIS, T_H2D, T_COUNT };
+
+struct DevPool {
+  std::vector<void*> ptrs;
+  size_t bytes = 0;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    const size_t sz = std::max<size_t>(count, 1) * sizeof(T);
+    if (cudaMalloc(&p, sz) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    ptrs.push_back(p);
+    bytes += sz;
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const T* src, size_t count, cudaStream_t st) {
+    T* d = alloc<T>(count);
+    if (d && count) cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, st);
+    return d;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+    bytes = 0;
+  }
+};
+
+struct PhaseTimer {
+  struct Span {
+    cudaEvent_t a, b;
+    int cat;
+  };
+  std::vector<Span> open_spans;
+  std::vector<cudaEvent_t> pool;
+  double total[T_COUNT] = {0};
+  bool enabled = true;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void begin(int cat, cudaStream_t st) {
+    if (!enabled) return;
+    Span s{get(), get(), cat};
+    cudaEventRecord(s.a, st);
+    open_spans.push_back(s);
+  }
+  void end(cudaStream_t st) {
+    if (!enabled) return;
+    cudaEventRecord(open_spans.back().b, st);
+  }
+  void collect() {  // call after a stream sync
+    for (auto& s : open_spans) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, s.a, s.b) == cudaSuccess) total[s.cat] += ms * 1e-3;
+      pool.push_back(s.a);
+      pool.push_back(s.b);
+    }
+    open_spans.clear();
+  }
+  void release() {
+    collect();
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+  }
+};
+
+}  // namespace
+
+struct qs_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  std::string err;
+  DevPool cone_pool, prob_pool;
+  PhaseTimer tm;
+  i64 launches = 0;
+
+  // ---- cone layout
+  bool have_cones = false;
+  ConeLayout L{};
+  WtwPlan wp{};
+  std::vector<i64> q_host;
+  std::vector<int> soc_ptr_host;
+  i64 S = 0;            // scaling slots
+  i64* d_slot_start = nullptr;
+  double* cone_tmp = nullptr;  // [m] scratch of the unit entry points
+  double deg = 0.0;
+
+  // reduction scratch + scalars
+  GridRed gr{};
+  double* scalars = nullptr;       // device [SC_COUNT]
+  double* scalars_host = nullptr;  // pinned [SC_COUNT]
+
+  // ---- problem
+  bool have_problem = false;
+  i64 n = 0, p = 0, m = 0, N = 0;
+  qs_settings st{};
+  Csr Pf{}, At{}, Gt{}, Ar{}, Gr{};
+  double *c = nullptr, *b = nullptr, *hv = nullptr;
+  double norm_c = 0, norm_b = 0, norm_h = 0;
+  // KKT
+  i64 knnz = 0;
+  std::vector<i64> Kp_h, Ki_h, pos_h;
+  std::vector<double> Kx_h;
+  i64* d_Kp = nullptr;
+  int* d_Ki = nullptr;
+  double* d_Kx = nullptr;
+  i64* d_pos = nullptr;
+  bool direct_ok = false;
+  LinSys ls;
+  bool factored = false;
+  i64 n_factor = 0, n_solve = 0;
+  // ---- state
+  double *x = nullptr, *y = nullptr, *z = nullptr, *s = nullptr;
+  double *w = nullptr, *eta = nullptr, *wbar = nullptr, *lam = nullptr, *lam_sq = nullptr;
+  double *d = nullptr, *dcomp = nullptr, *wdz = nullptr, *ds = nullptr, *r_cone = nullptr, *w2vz = nullptr;
+  double *rhs = nullptr, *sol = nullptr, *xa = nullptr, *xb = nullptr, *ra = nullptr, *rb = nullptr, *dx = nullptr;
+  double* tmp_m = nullptr;
+};
+
+namespace {
+
+#define CK(h, call)                                                      \
+  do {                                                                   \
+    cudaError_t e_ = (call);                                             \
+    if (e_ != cudaSuccess) {                                             \
+      (h)->err = std::string(#call) + ": " + cudaGetErrorString(e_);     \
+      return QS_E_CUDA;                                                  \
+    }                                                                    \
+  } while (0)
+
+int fail(qs_handle* h, int code, const std::string& msg) {
+  h->err = msg;
+  return code;
+}
+
+int check_launch(qs_handle* h, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, QS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return QS_OK;
+}
+
+bool ensure_scratch(qs_handle* h) {
+  if (h->scalars) return true;
+  if (cudaMalloc((void**)&h->scalars, SC_COUNT * sizeof(double)) != cudaSuccess) return false;
+  cudaMemsetAsync(h->scalars, 0, SC_COUNT * sizeof(double), h->stream);
+  if (cudaMallocHost((void**)&h->scalars_host, SC_COUNT * sizeof(double)) != cudaSuccess) return false;
+  if (cudaMalloc((void**)&h->gr.partial, (size_t)QS_MAX_GRID * QS_RED_MAXK * sizeof(double)) != cudaSuccess)
+    return false;
+  if (cudaMalloc((void**)&h->gr.counter, sizeof(unsigned)) != cudaSuccess) return false;
+  cudaMemsetAsync(h->gr.counter, 0, sizeof(unsigned), h->stream);
+  return true;
+}
+
+int fetch_scalars(qs_handle* h) {
+  CK(h, cudaMemcpyAsync(h->scalars_host, h->scalars, SC_COUNT * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->tm.collect();
+  return QS_OK;
+}
+
+i64 flags_of(const double* sc) {
+  i64 f = 0;
+  if (sc[SC_FLAG_NOT_INTERIOR] != 0.0) f |= 1;
+  if (sc[SC_FLAG_NONFINITE] != 0.0) f |= 2;
+  if (sc[SC_FLAG_BAD_STEP] != 0.0) f |= 4;
+  if (sc[SC_PIVOT_NONFINITE] != 0.0) f |= 8;
+  return f;
+}
+
+void clear_flags(qs_handle* h) {
+  // SC_FLAG_NOT_INTERIOR .. SC_FLAG_BAD_STEP are contiguous
+  cudaMemsetAsync(h->scalars + SC_FLAG_NOT_INTERIOR, 0, 3 * sizeof(double), h->stream);
+  cudaMemsetAsync(h->scalars + SC_PIVOT_BUMPS, 0, 2 * sizeof(double), h->stream);
+}
+
+template <class T>
+std::vector<int> to_i32(const T* src, size_t count) {
+  std::vector<int> out(count);
+  for (size_t k = 0; k < count; ++k) out[k] = (int)src[k];
+  return out;
+}
+
+bool make_csr(qs_handle* h, Csr* M, i64 rows, i64 cols, const i64* ptr, const i64* idx, const double* val) {
+  const i64 nnz = ptr[rows];
+  std::vector<int> p32 = to_i32(ptr, rows + 1), i32 = to_i32(idx, nnz);
+  M->rows = (int)rows;
+  M->cols = (int)cols;
+  M->ptr = h->prob_pool.upload(p32.data(), p32.size(), h->stream);
+  M->idx = h->prob_pool.upload(i32.data(), i32.size(), h->stream);
+  M->val = h->prob_pool.upload(val, nnz, h->stream);
+  M->tpr = qsk_pick_tpr(nnz, rows);
+  cudaStreamSynchronize(h->stream);  // the int32 staging vectors die here
+  return M->ptr && M->idx && M->val;
+}
+
+int scatter_scaling(qs_handle* h, const double* w, const double* eta, const double* wbar) {
+  h->tm.begin(T_KKT, h->stream);
+  qsk_neg_wtw(h->wp, h->direct_ok ? 2 : 1, w, eta, wbar, h->d_pos, h->d_Kx, h->stream);
+  h->launches += 2;
+  h->tm.end(h->stream);
+  return check_launch(h, "neg_wtw scatter");
+}
+
+// solve_refine (ldl.py:135-166) on the device: result in h->sol.
+int solve_refined(qs_handle* h, const double* rhs) {
+  const i64 N = h->N;
+  cudaStream_t st = h->stream;
+  auto backsolve = [&](const double* r, double* out) {
+    h->tm.begin(T_SOLVE, st);
+    h->ls.solve(r, out, st);
+    h->tm.end(st);
+    h->launches += 3 + 2 * h->ls.S.nlevels;
+  };
+  auto residual = [&](const double* v, double* r, int slot) {
+    h->tm.begin(T_REFINE, st);
+    if (h->st.kkt_literal) {
+      // r = rhs - sym(K) v over the stored entries (the reference's form)
+      cudaMemsetAsync(r, 0, N * sizeof(double), st);
+      qsk_spmv_sym_upper_csc((int)N, h->d_Kp, h->d_Ki, h->d_Kx, v, r, st);
+      qsk_axpby(N, 1.0, rhs, -1.0, r, r, st);
+      qsk_absmax(N, r, h->scalars + slot, nullptr, h->gr, st);
+      h->launches += 3;
+    } else {
+      qsk_apply_w2(h->L, h->w, h->eta, h->wbar, v + h->n + h->p, h->w2vz, st);
+      KktResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr,
+                        v,         rhs,       h->w2vz,   r,     h->scalars, slot, h->gr};
+      qsk_kkt_residual(A, st);
+      h->launches += 2;
+    }
+    h->tm.end(st);
+  };
+  double* x = h->xa;
+  double* xn = h->xb;
+  double* r = h->ra;
+  double* r2 = h->rb;
+  backsolve(rhs, x);
+  if (h->st.refine_iters > 0) {
+    qsk_absmax(N, rhs, h->scalars + SC_TMP0, nullptr, h->gr, st);
+    residual(x, r, SC_TMP1);
+    h->launches += 1;
+    int rc = fetch_scalars(h);
+    if (rc) return rc;
+    const double stop = 1e-12 * (1.0 + h->scalars_host[SC_TMP0]);  // ldl.py:19,151
+    double rn = h->scalars_host[SC_TMP1];
+    if (!(fabs(rn) <= DBL_MAX)) return fail(h, QS_E_NUMERICAL, "non-finite triangular solve result");
+    for (i64 it = 0; it < h->st.refine_iters; ++it) {
+      if (rn <= stop) break;
+      backsolve(r, h->dx);
+      qsk_axpby(N, 1.0, x, 1.0, h->dx, xn, st);
+      residual(xn, r2, SC_TMP2);
+      h->launches += 1;
+      rc = fetch_scalars(h);
+      if (rc) return rc;
+      const double rn2 = h->scalars_host[SC_TMP2];
+      if (!(fabs(rn2) <= DBL_MAX)) return fail(h, QS_E_NUMERICAL, "non-finite refinement residual");
+      if (rn2 >= rn) break;
+      std::swap(x, xn);
+      std::swap(r, r2);
+      rn = rn2;
+    }
+  }
+  h->sol = x;
+  h->n_solve++;
+  return check_launch(h, "linear solve");
+}
+
+int do_factor(qs_handle* h) {
+  h->tm.begin(T_FACTOR, h->stream);
+  h->ls.factor(h->d_Kx, h->scalars, h->stream);
+  h->tm.end(h->stream);
+  h->launches += 2 + h->ls.S.nlevels;
+  h->n_factor++;
+  h->factored = true;
+  return check_launch(h, "factor");
+}
+
+void fill_residual_info(qs_handle* h, qs_residual_info* o) {
+  const double* sc = h->scalars_host;
+  o->norm_r_dual = sc[SC_NORM_RDUAL];
+  o->norm_r_eq = sc[SC_NORM_REQ];
+  o->norm_r_cone = sc[SC_NORM_RCONE];
+  o->gap = sc[SC_GAP];
+  o->objective = sc[SC_OBJ];
+  o->norm_Px = sc[SC_NORM_PX];
+  o->norm_Aty = sc[SC_NORM_ATY];
+  o->norm_Gtz = sc[SC_NORM_GTZ];
+  o->norm_c = h->norm_c;
+  o->norm_Ax = sc[SC_NORM_AX];
+  o->norm_b = h->norm_b;
+  o->norm_Gx = sc[SC_NORM_GX];
+  o->norm_h = h->norm_h;
+  o->norm_s = sc[SC_NORM_S];
+  o->mu = sc[SC_MU];
+  o->flags = flags_of(sc);
+}
+
+double inf_norm(const double* v, i64 n) {
+  double t = 0.0;
+  for (i64 k = 0; k < n; ++k) {
+    const double a = fabs(v[k]);
+    if (a > t || a != a) t = a;
+  }
+  return t;
+}
+
+}  // namespace
+
+// =============================================================== C ABI ======
+extern "C" {
+
+int qs_version(void) { return 100; }
+
+int qs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+const char* qs_global_error(void) { return g_error.c_str(); }
+
+qs_handle* qs_create(int device) {
+  int cnt = qs_device_count();
+  if (device < 0 || device >= cnt) {
+    g_error = "no CUDA device " + std::to_string(device) + " (visible devices: " + std::to_string(cnt) + ")";
+    return nullptr;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    g_error = "cudaSetDevice failed";
+    return nullptr;
+  }
+  qs_handle* h = new qs_handle();
+  h->device = device;
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess || !ensure_scratch(h)) {
+    g_error = std::string("stream/scratch creation failed: ") + cudaGetErrorString(cudaGetLastError());
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void qs_destroy(qs_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  h->tm.release();
+  h->ls.release();
+  h->cone_pool.release();
+  h->prob_pool.release();
+  if (h->scalars) cudaFree(h->scalars);
+  if (h->scalars_host) cudaFreeHost(h->scalars_host);
+  if (h->gr.partial) cudaFree(h->gr.partial);
+  if (h->gr.counter) cudaFree(h->gr.counter);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char* qs_last_error(qs_handle* h) { return h ? h->err.c_str() : g_error.c_str(); }
+
+int qs_set_stream(qs_handle* h, void* cuda_stream) {
+  if (!h) return QS_E_INVALID;
+  cudaStreamSynchronize(h->stream);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  h->stream = (cudaStream_t)cuda_stream;
+  h->own_stream = false;
+  return QS_OK;
+}
+
+int qs_sync(qs_handle* h) {
+  if (!h) return QS_E_INVALID;
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->tm.collect();
+  return QS_OK;
+}
+
+// ---------------------------------------------------------------- host-side
+int64_t qs_kkt_nnz(int64_t n, int64_t m, int64_t p, int64_t l, int64_t nsoc, const int64_t* q, const int64_t* Pp,
+                   const int64_t* Pi, int64_t nnzA, int64_t nnzG) {
+  KktDims d{n, p, m, l, nsoc, (const i64*)q};
+  return hs_kkt_nnz(d, (const i64*)Pp, (const i64*)Pi, nnzA, nnzG);
+}
+
+int64_t qs_kkt_slot_count(int64_t l, int64_t nsoc, const int64_t* q) {
+  KktDims d{0, 0, 0, l, nsoc, (const i64*)q};
+  return hs_slot_count(d);
+}
+
+int qs_kkt_assemble(int64_t n, int64_t m, int64_t p, int64_t l, int64_t nsoc, const int64_t* q, const int64_t* Pp,
+                    const int64_t* Pi, const double* Px, const int64_t* Ap, const int64_t* Ai, const double* Ax,
+                    const int64_t* Gp, const int64_t* Gi, const double* Gx, int64_t* Kp, int64_t* Ki, double* Kx,
+                    int64_t* nt_entry_positions, int64_t* nt_slot_offsets, int64_t* soc_slot_starts) {
+  i64 msum = l;
+  for (i64 k = 0; k < nsoc; ++k) msum += q[k];
+  if (msum != m) return QS_E_DIMENSION;
+  KktDims d{n, p, m, l, nsoc, (const i64*)q};
+  const i64 nnzA = Ap[n], nnzG = Gp[n];
+  std::vector<i64> Arp(p + 1), Ari(nnzA), Grp(m + 1), Gri(nnzG);
+  std::vector<double> Arx(nnzA), Grx(nnzG);
+  hs_transpose(p, n, (const i64*)Ap, (const i64*)Ai, Ax, Arp.data(), Ari.data(), Arx.data());
+  hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, Gx, Grp.data(), Gri.data(), Grx.data());
+  hs_kkt_assemble(d, (const i64*)Pp, (const i64*)Pi, Px, Arp.data(), Ari.data(), Arx.data(), Grp.data(), Gri.data(),
+                  Grx.data(), (i64*)Kp, (i64*)Ki, Kx, (i64*)nt_entry_positions, (i64*)nt_slot_offsets,
+                  (i64*)soc_slot_starts);
+  return QS_OK;
+}
+
+int qs_symbolic_stats(int64_t N, const int64_t* Kp, const int64_t* Ki, int64_t ordering, const int64_t* user_perm,
+                      int64_t ncliques, const int64_t* clique_start, const int64_t* clique_size, int64_t* out_perm,
+                      double* stats6) {
+  Symbolic S;
+  std::string err = hs_symbolic_cliques(N, (const i64*)Kp, (const i64*)Ki, (int)ordering, (const i64*)user_perm,
+                                        ncliques, (const i64*)clique_start, (const i64*)clique_size, &S);
+  if (!err.empty()) {
+    g_error = err;
+    return QS_E_INVALID;
+  }
+  if (out_perm)
+    for (i64 k = 0; k < N; ++k) out_perm[k] = S.perm[k];
+  if (stats6) {
+    stats6[0] = S.nsup;
+    stats6[1] = S.nlevels;
+    stats6[2] = (double)S.lnz;
+    stats6[3] = S.flops;
+    stats6[4] = S.max_nr;
+    stats6[5] = S.max_ns;
+  }
+  return QS_OK;
+}
+
+// --------------------------------------------------------------- cone layout
+int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_t big_threshold) {
+  if (!h) return QS_E_INVALID;
+  if (l < 0 || nsoc < 0) return fail(h, QS_E_INVALID, "negative cone dimension");
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  h->cone_pool.release();
+  if (big_threshold <= 0) big_threshold = 2048;
+  i64 m = l;
+  std::vector<int> ptr(nsoc + 1);
+  std::vector<int> small_ids, big_ids;
+  ptr[0] = (int)l;
+  for (i64 k = 0; k < nsoc; ++k) {
+    if (q[k] < 1) return fail(h, QS_E_INVALID, "every SOC dimension must be >= 1");
+    m += q[k];
+    if (m >= ((i64)1 << 31)) return fail(h, QS_E_DIMENSION, "m exceeds 2^31");
+    ptr[k + 1] = (int)m;
+    (q[k] > big_threshold ? big_ids : small_ids).push_back((int)k);
+  }
+  h->q_host.assign(q, q + nsoc);
+  h->soc_ptr_host = ptr;
+  ConeLayout& L = h->L;
+  L.m = (int)m;
+  L.l = (int)l;
+  L.nsoc = (int)nsoc;
+  L.soc_ptr = h->cone_pool.upload(ptr.data(), ptr.size(), h->stream);
+  L.nsmall = (int)small_ids.size();
+  L.nbig = (int)big_ids.size();
+  L.small_ids = big_ids.empty() ? nullptr : h->cone_pool.upload(small_ids.data(), small_ids.size(), h->stream);
+  L.big_ids = big_ids.empty() ? nullptr : h->cone_pool.upload(big_ids.data(), big_ids.size(), h->stream);
+  // lanes per small cone: largest power of two <= mean small-cone size / 2, clamped to [1, 32]
+  double mean = 0.0;
+  for (int k : small_ids) mean += (double)q[k];
+  mean = small_ids.empty() ? 1.0 : mean / small_ids.size();
+  int G = 1;
+  while (G < 32 && G * 4 <= mean) G <<= 1;
+  L.group = G;
+  h->deg = (double)(l + nsoc);
+  // -W'W plan: column tiles of ~QS_WTW_TILE block entries
+  WtwPlan& P = h->wp;
+  P.l = (int)l;
+  P.nsoc = (int)nsoc;
+  P.m = (int)m;
+  P.soc_ptr = L.soc_ptr;
+  std::vector<int> cone_of_col(m - l), tile_ptr;
+  std::vector<i64> slot_start(nsoc);
+  i64 slot = l, acc = 0;
+  tile_ptr.push_back((int)l);
+  for (i64 k = 0; k < nsoc; ++k) {
+    slot_start[k] = slot;
+    slot += q[k] * (q[k] + 1) / 2;
+    for (i64 j = 0; j < q[k]; ++j) {
+      const i64 col = ptr[k] + j;
+      cone_of_col[col - l] = (int)k;
+      acc += j + 1;
+      if (acc >= QS_WTW_TILE) {
+        tile_ptr.push_back((int)(col + 1));
+        acc = 0;
+      }
+    }
+  }
+  if (tile_ptr.back() != (int)m) tile_ptr.push_back((int)m);
+  h->S = slot;
+  P.ntiles = (int)tile_ptr.size() - 1;
+  P.cone_of_col = h->cone_pool.upload(cone_of_col.data(), cone_of_col.size(), h->stream);
+  P.tile_ptr = h->cone_pool.upload(tile_ptr.data(), tile_ptr.size(), h->stream);
+  h->d_slot_start = h->cone_pool.upload(slot_start.data(), slot_start.size(), h->stream);
+  P.slot_start = h->d_slot_start;
+  P.kp_conic = nullptr;
+  P.c4 = h->cone_pool.alloc<double>(nsoc);
+  P.e2 = h->cone_pool.alloc<double>(nsoc);
+  h->cone_tmp = h->cone_pool.alloc<double>(m);
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (!L.soc_ptr || !P.cone_of_col || !P.tile_ptr || !P.c4 || !P.e2 || !h->cone_tmp)
+    return fail(h, QS_E_MEMORY, "cone layout alloc");
+  h->have_cones = true;
+  return QS_OK;
+}
+
+// ------------------------------------------------------- per-kernel entries
+#define NEED_CONES(h)                                                       \
+  if (!(h) || !(h)->have_cones) return (h) ? fail(h, QS_E_INVALID, "qs_set_cones first") : QS_E_INVALID; \
+  cudaSetDevice((h)->device);
+
+int qs_nt_scaling(qs_handle* h, const double* s, const double* z, double* w, double* eta, double* wbar, double* lam,
+                  double* lam_sq, int* not_interior_host) {
+  NEED_CONES(h)
+  if (not_interior_host) cudaMemsetAsync(h->scalars + SC_FLAG_NOT_INTERIOR, 0, sizeof(double), h->stream);
+  qsk_nt_scaling(h->L, s, z, w, eta, wbar, lam, lam_sq, h->scalars, h->stream);
+  h->launches++;
+  int rc = check_launch(h, "nt_scaling");
+  if (rc || !not_interior_host) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  *not_interior_host = h->scalars_host[SC_FLAG_NOT_INTERIOR] != 0.0;
+  return QS_OK;
+}
+
+int qs_apply_w(qs_handle* h, const double* w, const double* eta, const double* wbar, const double* u, double* out,
+               int inverse) {
+  NEED_CONES(h)
+  qsk_apply_w(h->L, w, eta, wbar, u, out, inverse, h->stream);
+  h->launches++;
+  return check_launch(h, "apply_w");
+}
+
+int qs_jordan_product(qs_handle* h, const double* u, const double* v, double* out) {
+  NEED_CONES(h)
+  qsk_jordan_product(h->L, u, v, out, h->stream);
+  h->launches++;
+  return check_launch(h, "jordan_product");
+}
+
+int qs_jordan_divide(qs_handle* h, const double* lam, const double* v, double* out) {
+  NEED_CONES(h)
+  qsk_jordan_divide(h->L, lam, v, out, h->stream);
+  h->launches++;
+  return check_launch(h, "jordan_divide");
+}
+
+int qs_max_step(qs_handle* h, const double* u, const double* du, double* step_host, double* violation_host) {
+  NEED_CONES(h)
+  qsk_max_step(h->L, u, du, h->scalars, SC_TMP0, SC_TMP1, h->gr, h->stream);
+  h->launches++;
+  int rc = check_launch(h, "max_step");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  if (step_host) *step_host = h->scalars_host[SC_TMP0];
+  if (violation_host) *violation_host = h->scalars_host[SC_TMP1];
+  return QS_OK;
+}
+
+int qs_bring_to_interior(qs_handle* h, const double* u, double scale, double* out, double* alpha_host) {
+  NEED_CONES(h)
+  // violation of scale*u, then the shift (cones.py:302-311)
+  double* t = h->cone_tmp;
+  qsk_axpby(h->L.m, scale, u, 0.0, nullptr, t, h->stream);
+  qsk_max_step(h->L, t, nullptr, h->scalars, -1, SC_SHIFT, h->gr, h->stream);
+  qsk_shift(h->L, t, out, h->scalars, SC_SHIFT, 1.0, h->stream);
+  h->launches += 3;
+  int rc = check_launch(h, "bring_to_interior");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (alpha_host) *alpha_host = h->scalars_host[SC_SHIFT];
+  return rc;
+}
+
+int qs_compute_mu(qs_handle* h, const double* s, const double* z, double* mu_host) {
+  NEED_CONES(h)
+  qsk_dot(h->L.m, s, z, 1.0 / h->deg, h->scalars + SC_TMP0, h->gr, h->stream);
+  h->launches++;
+  int rc = check_launch(h, "compute_mu");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (mu_host) *mu_host = h->scalars_host[SC_TMP0];
+  return rc;
+}
+
+int qs_neg_wtw(qs_handle* h, int mode, const double* w, const double* eta, const double* wbar,
+               const int64_t* soc_slot_starts_dev, const int64_t* positions_dev, const int64_t* kp_conic_dev,
+               double* out) {
+  NEED_CONES(h)
+  if (mode < 0 || mode > 2) return fail(h, QS_E_INVALID, "mode must be 0, 1 or 2");
+  WtwPlan P = h->wp;
+  if (soc_slot_starts_dev) P.slot_start = (const i64*)soc_slot_starts_dev;
+  if (mode == 1 && !positions_dev) return fail(h, QS_E_INVALID, "mode 1 needs the positions map");
+  if (mode == 2) {
+    if (!kp_conic_dev) return fail(h, QS_E_INVALID, "mode 2 needs kp_conic");
+    P.kp_conic = (const i64*)kp_conic_dev;
+  }
+  qsk_neg_wtw(P, mode, w, eta, wbar, (const i64*)positions_dev, out, h->stream);
+  h->launches += 2;
+  return check_launch(h, "neg_wtw");
+}
+
+int qs_spmv_csr(qs_handle* h, int64_t rows, int64_t cols, const int32_t* ptr, const int32_t* idx, const double* val,
+                const double* x, double* y, int accumulate) {
+  if (!h) return QS_E_INVALID;
+  cudaSetDevice(h->device);
+  int nnz_last = 0;
+  CK(h, cudaMemcpyAsync(&nnz_last, ptr + rows, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  Csr M{(int)rows, (int)cols, ptr, idx, val, qsk_pick_tpr(nnz_last, rows)};
+  qsk_spmv_csr(M, x, y, accumulate, h->stream);
+  h->launches++;
+  return check_launch(h, "spmv_csr");
+}
+
+int qs_spmv_sym_upper(qs_handle* h, int64_t ncols, const int64_t* colptr, const int32_t* rowidx, const double* val,
+                      const double* x, double* out) {
+  if (!h) return QS_E_INVALID;
+  cudaSetDevice(h->device);
+  qsk_spmv_sym_upper_csc((int)ncols, (const i64*)colptr, rowidx, val, x, out, h->stream);
+  h->launches++;
+  return check_launch(h, "spmv_sym_upper");
+}
+
+// ------------------------------------------------------------------- setup
+int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t nsoc, const int64_t* q,
+             const int64_t* Pp, const int64_t* Pi, const double* Px, const int64_t* Ap, const int64_t* Ai,
+             const double* Ax, const int64_t* Gp, const int64_t* Gi, const double* Gx, const double* c,
+             const double* b, const double* hvec, const qs_settings* settings, const int64_t* user_perm) {
+  if (!h || !settings) return QS_E_INVALID;
+  if (h->have_problem) return fail(h, QS_E_INVALID, "handle already set up");
+  cudaSetDevice(h->device);
+  const auto t_begin = std::chrono::steady_clock::now();
+  h->st = *settings;
+  if (n < 1 || m < 1 || p < 0) return fail(h, QS_E_DIMENSION, "need n >= 1, m >= 1, p >= 0");
+  int rc = qs_set_cones(h, l, nsoc, q, 0);
+  if (rc) return rc;
+  if (h->L.m != m) return fail(h, QS_E_DIMENSION, "cone dimensions do not sum to m");
+  h->n = n;
+  h->p = p;
+  h->m = m;
+  h->N = n + p + m;
+  const i64 N = h->N;
+  cudaStream_t st = h->stream;
+  // ---- row views
+  const i64 nnzA = Ap[n], nnzG = Gp[n], nnzP = Pp[n];
+  std::vector<i64> Arp(p + 1), Ari(nnzA), Grp(m + 1), Gri(nnzG);
+  std::vector<double> Arx(nnzA), Grx(nnzG);
+  hs_transpose(p, n, (const i64*)Ap, (const i64*)Ai, Ax, Arp.data(), Ari.data(), Arx.data());
+  hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, Gx, Grp.data(), Gri.data(), Grx.data());
+  // Pf = P + P' - diag(P), rows ascending
+  std::vector<i64> Pfp(n + 1, 0);
+  for (i64 j = 0; j < n; ++j)
+    for (i64 k = Pp[j]; k < Pp[j + 1]; ++k) {
+      const i64 i = Pi[k];
+      if (i > j) return fail(h, QS_E_INVALID, "P has an entry below the diagonal");
+      Pfp[i + 1]++;
+      if (i != j) Pfp[j + 1]++;
+    }
+  for (i64 r = 0; r < n; ++r) Pfp[r + 1] += Pfp[r];
+  std::vector<i64> Pfi(Pfp[n]);
+  std::vector<double> Pfx(Pfp[n]);
+  {
+    std::vector<i64> next(Pfp.begin(), Pfp.end() - 1);
+    for (i64 j = 0; j < n; ++j) {
+      for (i64 k = Pp[j]; k < Pp[j + 1]; ++k) {  // row j receives its cols i < j (and the diagonal)
+        const i64 i = Pi[k];
+        Pfi[next[j]] = i;
+        Pfx[next[j]++] = Px[k];
+      }
+      for (i64 k = Pp[j]; k < Pp[j + 1]; ++k) {  // rows i < j receive col j
+        const i64 i = Pi[k];
+        if (i == j) continue;
+        Pfi[next[i]] = j;
+        Pfx[next[i]++] = Px[k];
+      }
+    }
+  }
+  // ---- KKT system (host), then to the device
+  KktDims dims{n, p, m, l, nsoc, (const i64*)q};
+  h->knnz = hs_kkt_nnz(dims, (const i64*)Pp, (const i64*)Pi, nnzA, nnzG);
+  if (h->knnz >= ((i64)1 << 31)) return fail(h, QS_E_DIMENSION, "KKT nonzeros exceed 2^31");
+  h->Kp_h.resize(N + 1);
+  h->Ki_h.resize(h->knnz);
+  h->Kx_h.resize(h->knnz);
+  h->pos_h.resize(h->S);
+  std::vector<i64> soc_starts(nsoc), view_off(nsoc + 2);
+  hs_kkt_assemble(dims, (const i64*)Pp, (const i64*)Pi, Px, Arp.data(), Ari.data(), Arx.data(), Grp.data(),
+                  Gri.data(), Grx.data(), h->Kp_h.data(), h->Ki_h.data(), h->Kx_h.data(), h->pos_h.data(),
+                  view_off.data(), soc_starts.data());
+  const auto t_h2d = std::chrono::steady_clock::now();
+  bool ok = make_csr(h, &h->Pf, n, n, Pfp.data(), Pfi.data(), Pfx.data()) &&
+            make_csr(h, &h->At, n, p, (const i64*)Ap, (const i64*)Ai, Ax) &&
+            make_csr(h, &h->Gt, n, m, (const i64*)Gp, (const i64*)Gi, Gx) &&
+            make_csr(h, &h->Ar, p, n, Arp.data(), Ari.data(), Arx.data()) &&
+            make_csr(h, &h->Gr, m, n, Grp.data(), Gri.data(), Grx.data());
+  if (!ok) return fail(h, QS_E_MEMORY, "out of device memory for the problem matrices");
+  // one lane-group width for the whole dual range (three products per row)
+  h->Pf.tpr = qsk_pick_tpr(std::max(std::max(nnzP * 2, nnzA), nnzG), n);
+  h->At.tpr = h->Gt.tpr = h->Pf.tpr;
+  h->c = h->prob_pool.upload(c, n, st);
+  h->b = h->prob_pool.upload(b, p, st);
+  h->hv = h->prob_pool.upload(hvec, m, st);
+  h->norm_c = inf_norm(c, n);
+  h->norm_b = inf_norm(b, p);
+  h->norm_h = inf_norm(hvec, m);
+  {
+    std::vector<int> ki32 = to_i32(h->Ki_h.data(), h->Ki_h.size());
+    h->d_Kp = h->prob_pool.upload(h->Kp_h.data(), h->Kp_h.size(), st);
+    h->d_Ki = h->prob_pool.upload(ki32.data(), ki32.size(), st);
+    h->d_Kx = h->prob_pool.upload(h->Kx_h.data(), h->Kx_h.size(), st);
+    h->d_pos = h->prob_pool.upload(h->pos_h.data(), h->pos_h.size(), st);
+    CK(h, cudaStreamSynchronize(st));
+  }
+  if (!h->c || !h->b || !h->hv || !h->d_Kp || !h->d_Ki || !h->d_Kx || !h->d_pos)
+    return fail(h, QS_E_MEMORY, "out of device memory for the KKT system");
+  h->wp.kp_conic = h->d_Kp + n + p + 1;
+  // closed-form map == explicit map?
+  {
+    int* flag = h->prob_pool.alloc<int>(1);
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    qsk_check_direct_map(h->wp, h->d_pos, flag, st);
+    int bad = 1;
+    CK(h, cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaStreamSynchronize(st));
+    h->direct_ok = (bad == 0);
+  }
+  // ---- state vectors
+  DevPool& P = h->prob_pool;
+#define ALLOC(field, count)                  \
+  h->field = P.alloc<double>(count);         \
+  if (!h->field) return fail(h, QS_E_MEMORY, "out of device memory for the iterate");
+  ALLOC(x, n) ALLOC(y, p) ALLOC(z, m) ALLOC(s, m)
+  ALLOC(w, l) ALLOC(eta, nsoc) ALLOC(wbar, m) ALLOC(lam, m) ALLOC(lam_sq, m)
+  ALLOC(d, m) ALLOC(dcomp, m) ALLOC(wdz, m) ALLOC(ds, m) ALLOC(r_cone, m) ALLOC(w2vz, m) ALLOC(tmp_m, m)
+  ALLOC(rhs, N) ALLOC(xa, N) ALLOC(xb, N) ALLOC(ra, N) ALLOC(rb, N) ALLOC(dx, N)
+#undef ALLOC
+  cudaMemsetAsync(h->wbar, 0, m * sizeof(double), st);
+  h->sol = h->xa;
+  h->tm.total[T_H2D] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_h2d).count();
+  // ---- factorisation analysis; the SOC blocks are cliques of the pattern
+  std::vector<i64> cstart(nsoc), csize(nsoc);
+  for (i64 k = 0; k < nsoc; ++k) {
+    cstart[k] = n + p + h->soc_ptr_host[k];
+    csize[k] = q[k];
+  }
+  std::string err = h->ls.analyze(N, h->Kp_h.data(), h->Ki_h.data(), h->d_Kp, h->d_Ki, (int)h->st.ordering,
+                                  (const i64*)user_perm, nsoc, cstart.data(), csize.data(), n, h->st.static_reg, st);
+  if (!err.empty()) return fail(h, err.find("memory") != std::string::npos ? QS_E_MEMORY : QS_E_INVALID, err);
+  h->tm.total[T_ANALYSIS] += h->ls.analysis_seconds;
+  h->have_problem = true;
+  (void)t_begin;
+  return QS_OK;
+}
+
+#define NEED_PROBLEM(h)                                                                                     \
+  if (!(h) || !(h)->have_problem) return (h) ? fail(h, QS_E_INVALID, "qs_setup first") : QS_E_INVALID;       \
+  cudaSetDevice((h)->device);
+
+int64_t qs_kkt_size(qs_handle* h, int64_t* nnz, int64_t* slots) {
+  if (!h || !h->have_problem) return -1;
+  if (nnz) *nnz = h->knnz;
+  if (slots) *slots = h->S;
+  return h->N;
+}
+
+int qs_get_kkt(qs_handle* h, int64_t* Kp, int64_t* Ki, double* Kx, int64_t* positions) {
+  NEED_PROBLEM(h)
+  if (Kp) memcpy(Kp, h->Kp_h.data(), h->Kp_h.size() * sizeof(i64));
+  if (Ki) memcpy(Ki, h->Ki_h.data(), h->Ki_h.size() * sizeof(i64));
+  if (positions) memcpy(positions, h->pos_h.data(), h->pos_h.size() * sizeof(i64));
+  if (Kx) {  // current device values
+    CK(h, cudaMemcpyAsync(Kx, h->d_Kx, h->knnz * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
+  return QS_OK;
+}
+
+int qs_linsys_update_identity(qs_handle* h) {
+  NEED_PROBLEM(h)
+  // identity_scaling (cones.py:146-156): w = 1, eta = 1, wbar = e on the SOC heads, lam = e
+  std::vector<double> one(std::max<i64>(std::max<i64>(h->L.l, h->L.nsoc), 1), 1.0), e(h->m, 0.0);
+  for (int k = 0; k < h->L.nsoc; ++k) e[h->soc_ptr_host[k]] = 1.0;
+  CK(h, cudaMemcpyAsync(h->w, one.data(), h->L.l * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->eta, one.data(), h->L.nsoc * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->wbar, e.data(), h->m * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  for (int i = 0; i < h->L.l; ++i) e[i] = 1.0;
+  CK(h, cudaMemcpyAsync(h->lam, e.data(), h->m * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  int rc = scatter_scaling(h, h->w, h->eta, h->wbar);
+  CK(h, cudaStreamSynchronize(h->stream));
+  return rc;
+}
+
+int qs_linsys_update(qs_handle* h) {
+  NEED_PROBLEM(h)
+  return scatter_scaling(h, h->w, h->eta, h->wbar);
+}
+
+int qs_linsys_factor(qs_handle* h) {
+  NEED_PROBLEM(h)
+  return do_factor(h);
+}
+
+int qs_linsys_solve(qs_handle* h, const double* rhs_host, double* sol_host) {
+  NEED_PROBLEM(h)
+  if (!h->factored) return fail(h, QS_E_INVALID, "factor() must run before solve()");
+  CK(h, cudaMemcpyAsync(h->rhs, rhs_host, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  int rc = solve_refined(h, h->rhs);
+  if (rc) return rc;
+  CK(h, cudaMemcpyAsync(sol_host, h->sol, h->N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  for (i64 k = 0; k < h->N; ++k)
+    if (!(fabs(sol_host[k]) <= DBL_MAX)) return fail(h, QS_E_NUMERICAL, "non-finite linear-system solution");
+  return QS_OK;
+}
+
+// initialize_iterate (ipm.py:135-156)
+int qs_initialize_iterate(qs_handle* h, double* mu_host) {
+  NEED_PROBLEM(h)
+  cudaStream_t st = h->stream;
+  const i64 n = h->n, p = h->p, m = h->m;
+  clear_flags(h);
+  int rc = qs_linsys_update_identity(h);
+  if (rc) return rc;
+  rc = do_factor(h);
+  if (rc) return rc;
+  // rhs = (-c, b, h)
+  qsk_axpby(n, -1.0, h->c, 0.0, nullptr, h->rhs, st);
+  CK(h, cudaMemcpyAsync(h->rhs + n, h->b, p * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(h, cudaMemcpyAsync(h->rhs + n + p, h->hv, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  rc = solve_refined(h, h->rhs);
+  if (rc) return rc;
+  CK(h, cudaMemcpyAsync(h->x, h->sol, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(h, cudaMemcpyAsync(h->y, h->sol + n, p * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  // s = bring_to_interior(-z~)
+  h->tm.begin(T_CONE, st);
+  qsk_axpby(m, -1.0, h->sol + n + p, 0.0, nullptr, h->tmp_m, st);
+  qsk_max_step(h->L, h->tmp_m, nullptr, h->scalars, -1, SC_SHIFT, h->gr, st);
+  qsk_shift(h->L, h->tmp_m, h->s, h->scalars, SC_SHIFT, 1.0, st);
+  h->tm.end(st);
+  // rhs = (-c, 0, 0)
+  CK(h, cudaMemsetAsync(h->rhs + n, 0, (p + m) * sizeof(double), st));
+  rc = solve_refined(h, h->rhs);
+  if (rc) return rc;
+  h->tm.begin(T_CONE, st);
+  qsk_max_step(h->L, h->sol + n + p, nullptr, h->scalars, -1, SC_SHIFT, h->gr, st);
+  qsk_shift(h->L, h->sol + n + p, h->z, h->scalars, SC_SHIFT, 1.0, st);
+  qsk_dot((int)m, h->s, h->z, 1.0 / h->deg, h->scalars + SC_MU, h->gr, st);
+  h->tm.end(st);
+  h->launches += 7;
+  rc = check_launch(h, "initialize_iterate");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  const double mu = h->scalars_host[SC_MU];
+  if (mu_host) *mu_host = mu;
+  if (!(fabs(mu) <= DBL_MAX)) return fail(h, QS_E_NUMERICAL, "non-finite initial iterate");
+  if (h->scalars_host[SC_PIVOT_NONFINITE] != 0.0) return fail(h, QS_E_NUMERICAL, "non-finite pivot during LDL' factorization");
+  return QS_OK;
+}
+
+// compute_residuals (ipm.py:70-103)
+int qs_residuals(qs_handle* h, qs_residual_info* out) {
+  NEED_PROBLEM(h)
+  h->tm.begin(T_RESID, h->stream);
+  ResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->x, h->y, h->z, h->s,
+                 h->c,      h->b,      h->hv,     h->rhs, h->r_cone, h->scalars, h->gr};
+  qsk_residuals(A, h->stream);
+  h->tm.end(h->stream);
+  h->launches++;
+  int rc = check_launch(h, "residuals");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  if (out) fill_residual_info(h, out);
+  if (h->scalars_host[SC_FLAG_NONFINITE] != 0.0) return fail(h, QS_E_NUMERICAL, "non-finite residuals");
+  return QS_OK;
+}
+
+// ipm_step (ipm.py:159-235).  qs_residuals must have run on the current iterate
+// (rhs[0:n+p] and r_cone hold -r_dual, -r_eq, r_cone).
+int qs_step(qs_handle* h, qs_step_info* out) {
+  NEED_PROBLEM(h)
+  cudaStream_t st = h->stream;
+  const ConeLayout& L = h->L;
+  const i64 n = h->n, p = h->p, m = h->m;
+  clear_flags(h);
+  h->tm.begin(T_CONE, st);
+  qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->scalars, st);
+  h->tm.end(st);
+  int rc = scatter_scaling(h, h->w, h->eta, h->wbar);
+  if (rc) return rc;
+  rc = do_factor(h);
+  if (rc) return rc;
+  // predictor: d_comp = -lam o lam
+  h->tm.begin(T_CONE, st);
+  qsk_rhs_cone(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, -1.0, h->r_cone, h->d, h->rhs + n + p, st);
+  h->tm.end(st);
+  rc = solve_refined(h, h->rhs);
+  if (rc) return rc;
+  h->tm.begin(T_CONE, st);
+  qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, h->wdz, h->ds, h->scalars, 0,
+                 h->st.step_fraction, h->gr, st);
+  qsk_mu_aff((int)m, h->s, h->z, h->ds, h->sol + n + p, h->deg, h->scalars, h->gr, st);
+  // corrector: d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a)
+  qsk_dcomp(L, h->w, h->eta, h->wbar, h->ds, h->wdz, h->lam_sq, h->dcomp, h->scalars, st);
+  qsk_rhs_cone(L, h->w, h->eta, h->wbar, h->lam, h->dcomp, 1.0, h->r_cone, h->d, h->rhs + n + p, st);
+  h->tm.end(st);
+  rc = solve_refined(h, h->rhs);
+  if (rc) return rc;
+  h->tm.begin(T_CONE, st);
+  qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, nullptr, h->ds, h->scalars, 1,
+                 h->st.step_fraction, h->gr, st);
+  qsk_update_iterate((int)n, (int)p, (int)m, h->x, h->y, h->z, h->s, h->sol, h->ds, h->deg, h->scalars, h->gr, st);
+  h->tm.end(st);
+  h->launches += 8;
+  rc = check_launch(h, "ipm_step");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  const double* sc = h->scalars_host;
+  if (out) {
+    out->alpha = sc[SC_ALPHA];
+    out->alpha_affine = sc[SC_ALPHA_AFF];
+    out->sigma = sc[SC_SIGMA];
+    out->mu_affine = sc[SC_MU_AFF];
+    out->mu = sc[SC_MU];
+    out->step_s = sc[SC_STEP_S];
+    out->step_z = sc[SC_STEP_Z];
+    out->flags = flags_of(sc);
+  }
+  if (sc[SC_FLAG_NOT_INTERIOR] != 0.0) return fail(h, QS_E_NOT_INTERIOR, "point is not strictly inside the cone");
+  if (sc[SC_PIVOT_NONFINITE] != 0.0) return fail(h, QS_E_NUMERICAL, "non-finite pivot during LDL' factorization");
+  if (sc[SC_FLAG_BAD_STEP] != 0.0) return fail(h, QS_E_NUMERICAL, "non-positive or non-finite step length");
+  if (sc[SC_FLAG_NONFINITE] != 0.0) return fail(h, QS_E_NUMERICAL, "non-finite iterate");
+  return QS_OK;
+}
+
+int qs_get_iterate(qs_handle* h, double* x, double* y, double* z, double* s) {
+  NEED_PROBLEM(h)
+  cudaStream_t st = h->stream;
+  if (x) CK(h, cudaMemcpyAsync(x, h->x, h->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (y) CK(h, cudaMemcpyAsync(y, h->y, h->p * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (z) CK(h, cudaMemcpyAsync(z, h->z, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (s) CK(h, cudaMemcpyAsync(s, h->s, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  return QS_OK;
+}
+
+int qs_set_iterate(qs_handle* h, const double* x, const double* y, const double* z, const double* s) {
+  NEED_PROBLEM(h)
+  cudaStream_t st = h->stream;
+  if (x) CK(h, cudaMemcpyAsync(h->x, x, h->n * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (y) CK(h, cudaMemcpyAsync(h->y, y, h->p * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (z) CK(h, cudaMemcpyAsync(h->z, z, h->m * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (s) CK(h, cudaMemcpyAsync(h->s, s, h->m * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(h, cudaStreamSynchronize(st));
+  return QS_OK;
+}
+
+int qs_get_scaling(qs_handle* h, double* w, double* eta, double* wbar, double* lam) {
+  NEED_PROBLEM(h)
+  cudaStream_t st = h->stream;
+  if (w) CK(h, cudaMemcpyAsync(w, h->w, h->L.l * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (eta) CK(h, cudaMemcpyAsync(eta, h->eta, h->L.nsoc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (wbar) CK(h, cudaMemcpyAsync(wbar, h->wbar, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (lam) CK(h, cudaMemcpyAsync(lam, h->lam, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  return QS_OK;
+}
+
+int qs_set_scaling(qs_handle* h, const double* w, const double* eta, const double* wbar, const double* lam) {
+  NEED_PROBLEM(h)
+  cudaStream_t st = h->stream;
+  if (w) CK(h, cudaMemcpyAsync(h->w, w, h->L.l * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (eta) CK(h, cudaMemcpyAsync(h->eta, eta, h->L.nsoc * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (wbar) CK(h, cudaMemcpyAsync(h->wbar, wbar, h->m * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (lam) CK(h, cudaMemcpyAsync(h->lam, lam, h->m * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(h, cudaStreamSynchronize(st));
+  return QS_OK;
+}
+
+int qs_get_counters(qs_handle* h, int64_t* n_factor, int64_t* n_solve, int64_t* n_launches) {
+  if (!h) return QS_E_INVALID;
+  if (n_factor) *n_factor = h->n_factor;
+  if (n_solve) *n_solve = h->n_solve;
+  if (n_launches) *n_launches = h->launches;
+  return QS_OK;
+}
+
+int qs_get_timers(qs_handle* h, double* timers8) {
+  if (!h) return QS_E_INVALID;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  h->tm.collect();
+  for (int k = 0; k < T_COUNT; ++k) timers8[k] = h->tm.total[k];
+  return QS_OK;
+}
+
+int qs_get_factor_stats(qs_handle* h, double* s8) {
+  NEED_PROBLEM(h)
+  const Symbolic& S = h->ls.S;
+  s8[0] = S.nsup;
+  s8[1] = S.nlevels;
+  s8[2] = (double)S.lnz;
+  s8[3] = S.flops;
+  s8[4] = S.max_nr;
+  s8[5] = S.max_ns;
+  s8[6] = (double)h->ls.device_bytes;
+  s8[7] = h->direct_ok ? 1.0 : 0.0;
+  return QS_OK;
+}
+
+int qs_time_kernel(qs_handle* h, int kernel_id, int reps, double* ms_host) {
+  NEED_PROBLEM(h)
+  if (reps < 1) reps = 1;
+  cudaStream_t st = h->stream;
+  const ConeLayout& L = h->L;
+  const i64 n = h->n, p = h->p, m = h->m;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto run = [&]() {
+    switch (kernel_id) {
+      case 0: qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->scalars, st); break;
+      case 1: qsk_neg_wtw(h->wp, 2, h->w, h->eta, h->wbar, h->d_pos, h->d_Kx, st); break;
+      case 2: qsk_neg_wtw(h->wp, 1, h->w, h->eta, h->wbar, h->d_pos, h->d_Kx, st); break;
+      case 3: qsk_rhs_cone(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, -1.0, h->r_cone, h->d, h->rhs + n + p, st); break;
+      case 4: qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, h->wdz, h->ds, h->scalars, 0,
+                             h->st.step_fraction, h->gr, st); break;
+      case 5: qsk_mu_aff((int)m, h->s, h->z, h->ds, h->sol + n + p, h->deg, h->scalars, h->gr, st); break;
+      case 6: qsk_dcomp(L, h->w, h->eta, h->wbar, h->ds, h->wdz, h->lam_sq, h->dcomp, h->scalars, st); break;
+      case 7: {
+        ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->x, h->y, h->z, h->s,
+                       h->c,   h->b,   h->hv,  h->rhs, h->r_cone, h->scalars, h->gr};
+        qsk_residuals(A, st);
+        break;
+      }
+      case 8: qsk_apply_w(L, h->w, h->eta, h->wbar, h->ds, h->tmp_m, 0, st); break;
+      case 9: qsk_jordan_product(L, h->lam, h->lam, h->tmp_m, st); break;
+      case 10: qsk_jordan_divide(L, h->lam, h->lam_sq, h->tmp_m, st); break;
+      case 11: qsk_max_step(L, h->s, h->ds, h->scalars, SC_TMP0, SC_TMP1, h->gr, st); break;
+      case 12: h->ls.factor(h->d_Kx, h->scalars, st); break;
+      case 13: h->ls.solve(h->rhs, h->dx, st); break;
+      case 14: {
+        qsk_apply_w2(L, h->w, h->eta, h->wbar, h->sol + n + p, h->w2vz, st);
+        KktResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr,
+                          h->sol, h->rhs, h->w2vz, h->rb, h->scalars, SC_TMP3, h->gr};
+        qsk_kkt_residual(A, st);
+        break;
+      }
+      default: break;
+    }
+  };
+  if (kernel_id < 0 || kernel_id > 14) return fail(h, QS_E_INVALID, "unknown kernel id");
+  run();  // warm-up
+  CK(h, cudaEventRecord(a, st));
+  for (int r = 0; r < reps; ++r) run();
+  CK(h, cudaEventRecord(b, st));
+  CK(h, cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (ms_host) *ms_host = (double)ms / reps;
+  return check_launch(h, "time_kernel");
+}
+
+}  // extern "C"

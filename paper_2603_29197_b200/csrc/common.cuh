@@ -1,0 +1,215 @@
+// Shared device-side building blocks for the qsocp sm_100a kernels.
+//
+// Layout conventions (mirrors the reference's flat conic vectors,
+// pkg/src/qsocp/cones.py:40-58): a conic vector has length m; the orthant
+// block is [0, l); second-order cone k occupies [soc_ptr[k], soc_ptr[k+1]) with
+// its head first.  All values fp64.  Indices are int32 on the device (m and
+// nnz are checked < 2^31 at setup); int64 only where the reference contract
+// exposes them (the slot -> position map).
+#pragma once
+#include <cuda_runtime.h>
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+
+typedef long long i64;
+
+#define QS_THREADS 256
+#define QS_MAX_GRID 4096  // every reducing kernel launches at most this many blocks
+#define QS_RED_MAXK 16    // widest grid reduction (values per block)
+#define QS_UNBOUNDED DBL_MAX  // _cone_kernels.py:13
+
+// ------------------------------------------------------------------ scalars
+// Device-resident scalar block of one solver instance.  Written by the last
+// block of the reducing kernels, read by later kernels and (once per
+// iteration) by the host through a pinned mirror.
+enum QsScalar {
+  SC_STEP_S = 0,
+  SC_STEP_Z,
+  SC_ALPHA_AFF,
+  SC_ALPHA,
+  SC_MU,
+  SC_MU_AFF,
+  SC_SIGMA,
+  SC_VIOL_S,
+  SC_VIOL_Z,
+  SC_FLAG_NOT_INTERIOR,  // nonzero: NT scaling / max-step pre-check failed
+  SC_FLAG_NONFINITE,     // nonzero: non-finite iterate / residual / step
+  SC_FLAG_BAD_STEP,      // nonzero: alpha <= 0 or non-finite
+  SC_GAP,
+  SC_OBJ,
+  SC_XPX,
+  SC_CX,
+  SC_NORM_PX,
+  SC_NORM_ATY,
+  SC_NORM_GTZ,
+  SC_NORM_AX,
+  SC_NORM_GX,
+  SC_NORM_S,
+  SC_NORM_RDUAL,
+  SC_NORM_REQ,
+  SC_NORM_RCONE,
+  SC_REFINE_RNORM,   // ||rhs - K x||_inf of the last refinement residual
+  SC_REFINE_NONFINITE,
+  SC_SHIFT,          // bring_to_interior: violation alpha
+  SC_TMP0,
+  SC_TMP1,
+  SC_TMP2,
+  SC_TMP3,
+  SC_PIVOT_BUMPS,
+  SC_PIVOT_NONFINITE,
+  SC_COUNT = 48
+};
+
+// --------------------------------------------------------------- cone layout
+struct ConeLayout {
+  int m, l, nsoc;
+  const int* soc_ptr;    // [nsoc+1]
+  int group;             // lanes cooperating on one small cone (1,2,4,...,32)
+  int nsmall;            // cones handled by lane groups
+  const int* small_ids;  // [nsmall] or nullptr when every cone is small
+  int nbig;              // cones handled by a whole CTA (dim > big threshold)
+  const int* big_ids;    // [nbig]
+};
+
+// ------------------------------------------------------------ group policies
+// A "group" is the set of threads that cooperates on one cone.  sum() is an
+// all-reduce: every thread of the group gets the same bits back.
+template <int G>
+struct LaneGroup {
+  static constexpr int kSize = G;
+  __device__ __forceinline__ int lane() const { return threadIdx.x & (G - 1); }
+  __device__ __forceinline__ int size() const { return G; }
+  // shuffles name only this group's lanes, so groups of one warp may diverge
+  __device__ __forceinline__ unsigned mask() const {
+    return G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (threadIdx.x & 31 & ~(G - 1)));
+  }
+  __device__ __forceinline__ double sum(double v) const {
+    const unsigned mk = mask();
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mk, v, o);
+    return v;
+  }
+};
+
+struct CtaGroup {
+  double* scratch;  // [32] shared
+  __device__ __forceinline__ int lane() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ double sum(double v) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();  // scratch may still be read from a previous sum()
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int w = 0; w < nw; ++w) t += scratch[w];
+    return t;
+  }
+};
+
+// ------------------------------------------------------- grid-wide reduction
+// Deterministic (fixed grid -> fixed order) reduction of K doubles across the
+// whole grid with the "last block finishes" pattern: each block publishes its
+// partials, takes a ticket, and the block drawing the last ticket combines all
+// partials in block order and runs `fin(result)` on thread 0.
+enum { RED_SUM = 0, RED_MIN = 1, RED_MAX = 2 };
+
+struct GridRed {
+  double* partial;    // [>= gridDim.x * K]
+  unsigned* counter;  // zero before the launch; left zero afterwards
+};
+
+__device__ __forceinline__ double qs_combine(double a, double b, int op) {
+  // NaN-propagating max/min so that non-finite data is never masked
+  if (op == RED_SUM) return a + b;
+  if (a != a) return a;
+  if (b != b) return b;
+  if (op == RED_MIN) return b < a ? b : a;
+  return b > a ? b : a;
+}
+
+__device__ __forceinline__ double qs_identity(int op) {
+  return op == RED_SUM ? 0.0 : (op == RED_MIN ? INFINITY : -INFINITY);
+}
+
+template <int K>
+struct RedOps {
+  int op[K];
+};
+
+template <int K>
+__device__ __forceinline__ void qs_block_reduce(double (&v)[K], const RedOps<K>& ops, double* sm /*[32*K]*/) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = qs_combine(x, __shfl_xor_sync(0xffffffffu, x, o), ops.op[k]);
+    v[k] = x;
+  }
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sm[w * K + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double x = sm[k];
+      for (int j = 1; j < nw; ++j) x = qs_combine(x, sm[j * K + k], ops.op[k]);
+      v[k] = x;
+    }
+  }
+}
+
+// After the call, thread 0 of exactly one block (the last to arrive) has run
+// fin(totals).  Every thread of every block must call this.
+template <int K, class Fin>
+__device__ __forceinline__ void qs_grid_reduce(double (&v)[K], const RedOps<K>& ops, GridRed gr, Fin fin) {
+  __shared__ double sm[32 * K];
+  __shared__ int last;
+  qs_block_reduce<K>(v, ops, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) gr.partial[(size_t)blockIdx.x * K + k] = v[k];
+    __threadfence();
+    const unsigned t = atomicInc(gr.counter, gridDim.x - 1);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = qs_identity(ops.op[k]);
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      acc[k] = qs_combine(acc[k], __ldcg(&gr.partial[(size_t)b * K + k]), ops.op[k]);
+  }
+  qs_block_reduce<K>(acc, ops, sm);
+  if (threadIdx.x == 0) fin(acc);
+}
+
+// ------------------------------------------------------------------- helpers
+__device__ __forceinline__ bool qs_finite(double v) { return fabs(v) <= DBL_MAX; }
+
+// Exit step of one second-order cone from the quadratic's coefficients
+// (a = du0^2 - |du1|^2, b = 2(u0 du0 - u1.du1), c = u0^2 - |u1|^2), branch for
+// branch as the reference (_cone_kernels.py:124-143).
+__device__ __forceinline__ double qs_soc_step(double a, double b, double c) {
+  if (a == 0.0) return (b < 0.0) ? -c / b : QS_UNBOUNDED;
+  const double disc = __dsub_rn(__dmul_rn(b, b), __dmul_rn(__dmul_rn(4.0, a), c));
+  if (a > 0.0 && disc < 0.0) return QS_UNBOUNDED;
+  const double sq = sqrt(disc);
+  const double den = (b >= 0.0) ? (-b - sq) : (-b + sq);
+  const double r1 = den / (2.0 * a);
+  const double r2 = (den != 0.0) ? 2.0 * c / den : QS_UNBOUNDED;
+  double step = QS_UNBOUNDED;
+  if (0.0 < r1 && r1 < step) step = r1;
+  if (0.0 < r2 && r2 < step) step = r2;
+  return step;
+}

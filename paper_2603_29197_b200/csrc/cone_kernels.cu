@@ -1,0 +1,760 @@
+// Cone algebra kernels: Nesterov-Todd scaling, W / W^-1 application, Jordan
+// product and division, max step to the boundary, interior violation, and the
+// fused per-iteration kernels built from them.
+//
+// One launch covers the whole product cone.  The grid is cut into three block
+// ranges: [orthant | small SOCs | big SOCs].
+//   * orthant: grid-stride elementwise, 128-bit (double2) accesses;
+//   * small SOCs: a power-of-two lane group (1..32 lanes, chosen from the mean
+//     cone size at setup) per cone, segmented reductions by xor-shuffles;
+//   * big SOCs (dim > threshold): one CTA per cone, shuffles + a shared-memory
+//     stage.
+// A cone is read once from HBM; later passes over the same cone hit L1/L2.
+//
+// Every op cites the reference lines whose arithmetic it reproduces
+// (paths relative to /root/reference/pkg/src/qsocp/).
+#include "cone_kernels.h"
+
+namespace {
+
+// ------------------------------------------------------------------ dispatch
+struct NoAcc {};
+
+template <int G, class Op>
+__global__ void __launch_bounds__(QS_THREADS) cone_kernel(ConeLayout L, Op op, int nb_orth, int nb_small, int nb_big) {
+  typename Op::Acc acc;
+  op.init(acc);
+  const int b = blockIdx.x;
+  if (b < nb_orth) {
+    op.orthant(acc, L, b * blockDim.x + threadIdx.x, nb_orth * blockDim.x);
+  } else if (b < nb_orth + nb_small) {
+    // lane groups stride over the small cones; groups of one warp may diverge
+    // (their shuffles name only their own lanes)
+    const int ngroups = nb_small * (QS_THREADS / G);
+    LaneGroup<G> g;
+    for (int gid = ((b - nb_orth) * blockDim.x + threadIdx.x) / G; gid < L.nsmall; gid += ngroups) {
+      const int k = L.small_ids ? L.small_ids[gid] : gid;
+      const int o = L.soc_ptr[k];
+      op.soc(acc, g, k, o, L.soc_ptr[k + 1] - o);
+    }
+  } else {
+    __shared__ double scratch[32];
+    CtaGroup g{scratch};
+    for (int id = b - nb_orth - nb_small; id < L.nbig; id += nb_big) {
+      const int k = L.big_ids[id];
+      const int o = L.soc_ptr[k];
+      op.soc(acc, g, k, o, L.soc_ptr[k + 1] - o);
+    }
+  }
+  op.finish(acc);
+}
+
+template <class Op>
+void launch(const ConeLayout& L, const Op& op, cudaStream_t st) {
+  const int cap = QS_MAX_GRID / 4;
+  int nb_orth = 0;
+  if (L.l > 0) {
+    nb_orth = (L.l / 2 + QS_THREADS - 1) / QS_THREADS;
+    if (nb_orth < 1) nb_orth = 1;
+    if (nb_orth > cap) nb_orth = cap;
+  }
+  const int G = L.group;
+  i64 nbs = L.nsmall > 0 ? ((i64)L.nsmall * G + QS_THREADS - 1) / QS_THREADS : 0;
+  if (nbs > 2 * cap) nbs = 2 * cap;
+  const int nb_small = (int)nbs;
+  const int nb_big = L.nbig > cap ? cap : L.nbig;
+  const int grid = nb_orth + nb_small + nb_big;
+  if (grid == 0) return;
+  switch (G) {
+    case 1: cone_kernel<1, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+    case 2: cone_kernel<2, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+    case 4: cone_kernel<4, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+    case 8: cone_kernel<8, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+    case 16: cone_kernel<16, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+    default: cone_kernel<32, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+  }
+}
+
+#define QS_EMPTY_GUARD(L) ((L).l == 0 && (L).nsoc == 0)
+
+// W u on one SOC (forward) or W^-1 u (inverse), _cone_kernels.py:56-74:
+//   dot = wbar0 u0 + sgn * sum wbar_t u_t ; out0 = scale (2 wbar0 dot - u0)
+//   out_t = scale (2 sgn wbar_t dot + u_t)
+__device__ __forceinline__ double w_head(double scale, double wb0, double dot, double u0) {
+  return scale * (2.0 * wb0 * dot - u0);
+}
+__device__ __forceinline__ double w_tail(double scale, double sgn, double wbt, double dot, double ut) {
+  return scale * (2.0 * sgn * wbt * dot + ut);
+}
+
+// ----------------------------------------------------------------- NT scaling
+// compute_nt_scaling (cones.py:159-184) + soc_nt_scaling (_cone_kernels.py:16-53)
+// fused with lam o lam (ipm.py:191, _cone_kernels.py:77-89).
+struct NtScalingOp {
+  const double* s;
+  const double* z;
+  double* w;
+  double* eta;
+  double* wbar;
+  double* lam;
+  double* lam_sq;  // may be null
+  double* scalars;
+  struct Acc {
+    int bad;
+  };
+  __device__ void init(Acc& a) const { a.bad = 0; }
+  __device__ void orthant(Acc& a, const ConeLayout& L, int tid, int nth) const {
+    const int l2 = L.l >> 1;
+    const double2* s2 = reinterpret_cast<const double2*>(s);
+    const double2* z2 = reinterpret_cast<const double2*>(z);
+    for (int i = tid; i < l2; i += nth) {
+      const double2 sv = s2[i], zv = z2[i];
+      if (sv.x <= 0.0 || sv.y <= 0.0 || zv.x <= 0.0 || zv.y <= 0.0) a.bad = 1;
+      double2 wv, lv;
+      wv.x = sqrt(sv.x / zv.x);
+      wv.y = sqrt(sv.y / zv.y);
+      lv.x = sqrt(sv.x * zv.x);
+      lv.y = sqrt(sv.y * zv.y);
+      reinterpret_cast<double2*>(w)[i] = wv;
+      reinterpret_cast<double2*>(lam)[i] = lv;
+      if (lam_sq) reinterpret_cast<double2*>(lam_sq)[i] = make_double2(lv.x * lv.x, lv.y * lv.y);
+    }
+    if ((L.l & 1) && tid == 0) {
+      const int i = L.l - 1;
+      const double sv = s[i], zv = z[i];
+      if (sv <= 0.0 || zv <= 0.0) a.bad = 1;
+      w[i] = sqrt(sv / zv);
+      const double lv = sqrt(sv * zv);
+      lam[i] = lv;
+      if (lam_sq) lam_sq[i] = lv * lv;
+    }
+  }
+  template <class Grp>
+  __device__ void soc(Acc& a, const Grp& g, int k, int o, int q) const {
+    const double s0 = q ? s[o] : 1.0, z0 = q ? z[o] : 1.0;
+    double ss = 0.0, zz = 0.0, sz = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double a1 = s[o + t], b1 = z[o + t];
+      ss += a1 * a1;
+      zz += b1 * b1;
+      sz += a1 * b1;
+    }
+    ss = g.sum(ss);
+    zz = g.sum(zz);
+    sz = g.sum(sz);
+    const double sres = s0 * s0 - ss, zres = z0 * z0 - zz;
+    // a cone that is not strictly interior raises the flag and writes nothing
+    // (the reference aborts with NotInterior, cones.py:182-183)
+    const bool ok = s0 > 0.0 && z0 > 0.0 && sres > 0.0 && zres > 0.0;
+    if (!ok && q) a.bad = 1;
+    if (!ok) q = 0;
+    const double sa = ok ? sqrt(sres) : 1.0, za = ok ? sqrt(zres) : 1.0;
+    const double gamma = sqrt((1.0 + (s0 * z0 + sz) / (sa * za)) / 2.0);
+    const double nt0 = (s0 / sa + z0 / za) / (2.0 * gamma);
+    const double den = sqrt(2.0 * (1.0 + nt0));
+    const double wb0 = (nt0 + 1.0) / den;
+    const double ek = sqrt(sa / za);
+    double wz = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double zt = z[o + t];
+      const double wbt = (s[o + t] / sa - zt / za) / (2.0 * gamma) / den;
+      wbar[o + t] = wbt;
+      wz += wbt * zt;
+    }
+    wz = g.sum(wz) + wb0 * z0;
+    const double lam0 = ek * (2.0 * wb0 * wz - z0);
+    double ll = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double zt = z[o + t];
+      const double wbt = (s[o + t] / sa - zt / za) / (2.0 * gamma) / den;
+      const double lt = ek * (2.0 * wbt * wz + zt);
+      lam[o + t] = lt;
+      ll += lt * lt;
+      if (lam_sq) lam_sq[o + t] = lam0 * lt + lam0 * lt;
+    }
+    ll = g.sum(ll);
+    if (g.lane() == 0 && q) {
+      wbar[o] = wb0;
+      eta[k] = ek;
+      lam[o] = lam0;
+      if (lam_sq) lam_sq[o] = lam0 * lam0 + ll;
+    }
+  }
+  __device__ void finish(Acc& a) const {
+    if (a.bad) scalars[SC_FLAG_NOT_INTERIOR] = 1.0;
+  }
+};
+
+// -------------------------------------------------------------- apply W / W^-1
+// apply_scaling (cones.py:192-212) + soc_apply_w (_cone_kernels.py:56-74)
+struct ApplyWOp {
+  const double* w;
+  const double* eta;
+  const double* wbar;
+  const double* u;
+  double* out;
+  int inverse;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) out[i] = inverse ? u[i] / w[i] : u[i] * w[i];
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double sgn = inverse ? -1.0 : 1.0;
+    double dot = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) dot += sgn * wbar[o + t] * u[o + t];
+    const double wb0 = q ? wbar[o] : 0.0, u0 = q ? u[o] : 0.0;
+    dot = wb0 * u0 + g.sum(dot);
+    const double e = q ? eta[k] : 1.0;
+    const double scale = inverse ? 1.0 / e : e;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = w_tail(scale, sgn, wbar[o + t], dot, u[o + t]);
+    if (g.lane() == 0 && q) out[o] = w_head(scale, wb0, dot, u0);
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// ------------------------------------------------------------- Jordan product
+// jordan_product (cones.py:215-228) + soc_jordan (_cone_kernels.py:77-89)
+struct JordanProductOp {
+  const double* u;
+  const double* v;
+  double* out;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) out[i] = u[i] * v[i];
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double u0 = q ? u[o] : 0.0, v0 = q ? v[o] : 0.0;
+    double dot = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double ut = u[o + t], vt = v[o + t];
+      dot += ut * vt;
+      out[o + t] = u0 * vt + v0 * ut;
+    }
+    dot = u0 * v0 + g.sum(dot);
+    if (g.lane() == 0 && q) out[o] = dot;
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// ------------------------------------------------------------ Jordan division
+// jordan_divide (cones.py:231-244) + soc_jordan_div (_cone_kernels.py:92-106)
+struct JordanDivideOp {
+  const double* lam;
+  const double* v;
+  double* out;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) out[i] = v[i] / lam[i];
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double a = q ? lam[o] : 1.0, v0 = q ? v[o] : 0.0;
+    double ll = 0.0, cross = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double lt = lam[o + t];
+      ll += lt * lt;
+      cross += lt * v[o + t];
+    }
+    ll = g.sum(ll);
+    cross = g.sum(cross);
+    const double u0 = (a * v0 - cross) / (a * a - ll);
+    for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = (v[o + t] - u0 * lam[o + t]) / a;
+    if (g.lane() == 0 && q) out[o] = u0;
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// ------------------------------------------------ max step + interior check
+// max_step_to_boundary (cones.py:247-272), check_interior/interior_violation
+// (cones.py:275-299), soc_max_step (_cone_kernels.py:109-146), soc_violation
+// (_cone_kernels.py:149-162).  Writes scalars[slot_step] and scalars[slot_viol].
+struct MaxStepOp {
+  const double* u;
+  const double* du;  // may be null: violation only
+  double* scalars;
+  int slot_step, slot_viol;
+  GridRed gr;
+  struct Acc {
+    double step, viol;
+  };
+  __device__ void init(Acc& a) const {
+    a.step = QS_UNBOUNDED;
+    a.viol = -INFINITY;
+  }
+  __device__ void orthant(Acc& a, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) {
+      const double ui = u[i];
+      a.viol = fmax(a.viol, -ui);
+      if (du) {
+        const double di = du[i];
+        if (di < 0.0) a.step = fmin(a.step, -ui / di);
+      }
+    }
+  }
+  template <class Grp>
+  __device__ void soc(Acc& acc, const Grp& g, int k, int o, int q) const {
+    double uu = 0.0, dd = 0.0, ud = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double ut = u[o + t];
+      uu += ut * ut;
+      if (du) {
+        const double dt = du[o + t];
+        dd += dt * dt;
+        ud += ut * dt;
+      }
+    }
+    uu = g.sum(uu);
+    if (du) {
+      dd = g.sum(dd);
+      ud = g.sum(ud);
+    }
+    if (q && g.lane() == 0) {
+      const double u0 = u[o];
+      acc.viol = fmax(acc.viol, sqrt(uu) - u0);
+      if (du) {
+        const double d0 = du[o];
+        acc.step = fmin(acc.step, qs_soc_step(d0 * d0 - dd, 2.0 * (u0 * d0 - ud), u0 * u0 - uu));
+      }
+    }
+  }
+  __device__ void finish(Acc& a) const {
+    double v[2] = {a.step, a.viol};
+    const RedOps<2> ops = {{RED_MIN, RED_MAX}};
+    double* sc = scalars;
+    const int ss = slot_step, sv = slot_viol;
+    qs_grid_reduce<2>(v, ops, gr, [=](double (&t)[2]) {
+      if (ss >= 0) sc[ss] = t[0];
+      if (sv >= 0) sc[sv] = t[1];
+    });
+  }
+};
+
+// ------------------------------------------------------------ shift interior
+// bring_to_interior (cones.py:302-311): out = u (+ (1 + alpha) e when the
+// violation alpha = scalars[slot] is >= 0).  scale = -1 negates u first (the
+// initial slack is -z~, ipm.py:146).
+struct ShiftOp {
+  const double* u;
+  double* out;
+  const double* scalars;
+  int slot;
+  double scale;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    const double alpha = scalars[slot];
+    const double add = (alpha < 0.0) ? 0.0 : 1.0 + alpha;
+    for (int i = tid; i < L.l; i += nth) {
+      const double v = scale * u[i];
+      out[i] = (alpha < 0.0) ? v : v + add;
+    }
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double alpha = scalars[slot];
+    const double add = 1.0 + alpha;
+    // tail: u + (1+alpha)*0.0 == u
+    for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = scale * u[o + t];
+    if (g.lane() == 0 && q) {
+      const double v = scale * u[o];
+      out[o] = (alpha < 0.0) ? v : v + add;
+    }
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// ------------------------------------------------- corrector complementarity
+// d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a)   (ipm.py:209-211)
+struct DcompOp {
+  const double* w;
+  const double* eta;
+  const double* wbar;
+  const double* ds_a;
+  const double* wdz_a;
+  const double* lam_sq;
+  double* dcomp;
+  const double* scalars;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    const double sm = scalars[SC_SIGMA] * scalars[SC_MU];
+    for (int i = tid; i < L.l; i += nth) {
+      const double winv = ds_a[i] / w[i];
+      dcomp[i] = sm - lam_sq[i] - winv * wdz_a[i];
+    }
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double sm = scalars[SC_SIGMA] * scalars[SC_MU];
+    const double wb0 = q ? wbar[o] : 0.0, u0 = q ? ds_a[o] : 0.0, y0 = q ? wdz_a[o] : 0.0;
+    const double scale = q ? 1.0 / eta[k] : 1.0;
+    double dot = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) dot += -1.0 * wbar[o + t] * ds_a[o + t];
+    dot = wb0 * u0 + g.sum(dot);
+    const double x0 = w_head(scale, wb0, dot, u0);  // (W^-1 ds_a)_0
+    double cr = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double xt = w_tail(scale, -1.0, wbar[o + t], dot, ds_a[o + t]);
+      const double yt = wdz_a[o + t];
+      cr += xt * yt;
+      dcomp[o + t] = 0.0 - lam_sq[o + t] - (x0 * yt + y0 * xt);
+    }
+    cr = x0 * y0 + g.sum(cr);
+    if (g.lane() == 0 && q) dcomp[o] = sm - lam_sq[o] - cr;
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// --------------------------------------------------- third RHS block (a-11)
+// d = lam \ (sign * dc) ; rhs_z = -r_cone - W d          (ipm.py:180-184)
+struct RhsConeOp {
+  const double* w;
+  const double* eta;
+  const double* wbar;
+  const double* lam;
+  const double* dc;
+  double sign;
+  const double* r_cone;
+  double* d;
+  double* rhs_z;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) {
+      const double di = (sign * dc[i]) / lam[i];
+      d[i] = di;
+      rhs_z[i] = -r_cone[i] - di * w[i];
+    }
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double a = q ? lam[o] : 1.0, v0 = q ? sign * dc[o] : 0.0;
+    double ll = 0.0, cross = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double lt = lam[o + t];
+      ll += lt * lt;
+      cross += lt * (sign * dc[o + t]);
+    }
+    ll = g.sum(ll);
+    cross = g.sum(cross);
+    const double d0 = (a * v0 - cross) / (a * a - ll);
+    const double wb0 = q ? wbar[o] : 0.0;
+    double dot = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) / a;
+      d[o + t] = dt;
+      dot += wbar[o + t] * dt;
+    }
+    dot = wb0 * d0 + g.sum(dot);
+    const double e = q ? eta[k] : 1.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) / a;
+      rhs_z[o + t] = -r_cone[o + t] - w_tail(e, 1.0, wbar[o + t], dot, dt);
+    }
+    if (g.lane() == 0 && q) {
+      d[o] = d0;
+      rhs_z[o] = -r_cone[o] - w_head(e, wb0, dot, d0);
+    }
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// ----------------------------------------- after the solve: ds and both steps
+// wdz = W dz ; ds = W (d - wdz)                                (ipm.py:187-188)
+// step_s = max_step(s, ds), step_z = max_step(z, dz)           (ipm.py:195-196 / 214-215)
+// final:  predictor  alpha_aff = min(1, step_s, step_z)        (ipm.py:197)
+//         corrector  alpha = min(1, step_fraction * min(..))   (ipm.py:216-218)
+struct PostSolveOp {
+  const double* w;
+  const double* eta;
+  const double* wbar;
+  const double* d;
+  const double* dz;
+  const double* s;
+  const double* z;
+  double* wdz;  // may be null (corrector does not need it)
+  double* ds;
+  double* scalars;
+  int corrector;
+  double step_fraction;
+  GridRed gr;
+  struct Acc {
+    double step_s, step_z, viol_s, viol_z;
+  };
+  __device__ void init(Acc& a) const {
+    a.step_s = a.step_z = QS_UNBOUNDED;
+    a.viol_s = a.viol_z = -INFINITY;
+  }
+  __device__ void orthant(Acc& a, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) {
+      const double wi = w[i], dzi = dz[i];
+      const double y = dzi * wi;
+      const double dsi = (d[i] - y) * wi;
+      if (wdz) wdz[i] = y;
+      ds[i] = dsi;
+      const double si = s[i], zi = z[i];
+      a.viol_s = fmax(a.viol_s, -si);
+      a.viol_z = fmax(a.viol_z, -zi);
+      if (dsi < 0.0) a.step_s = fmin(a.step_s, -si / dsi);
+      if (dzi < 0.0) a.step_z = fmin(a.step_z, -zi / dzi);
+    }
+  }
+  template <class Grp>
+  __device__ void soc(Acc& acc, const Grp& g, int k, int o, int q) const {
+    const double wb0 = q ? wbar[o] : 0.0, e = q ? eta[k] : 1.0;
+    const double dz0 = q ? dz[o] : 0.0, z0 = q ? z[o] : 1.0, s0 = q ? s[o] : 1.0, d0 = q ? d[o] : 0.0;
+    // pass 1: w.dz and the (z, dz) quadratic
+    double dot1 = 0.0, zz = 0.0, dd = 0.0, zd = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double dzt = dz[o + t], zt = z[o + t];
+      dot1 += wbar[o + t] * dzt;
+      zz += zt * zt;
+      dd += dzt * dzt;
+      zd += zt * dzt;
+    }
+    dot1 = wb0 * dz0 + g.sum(dot1);
+    zz = g.sum(zz);
+    dd = g.sum(dd);
+    zd = g.sum(zd);
+    const double y0 = w_head(e, wb0, dot1, dz0);
+    // pass 2: w.(d - wdz)
+    double dot2 = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double yt = w_tail(e, 1.0, wbar[o + t], dot1, dz[o + t]);
+      if (wdz) wdz[o + t] = yt;
+      dot2 += wbar[o + t] * (d[o + t] - yt);
+    }
+    const double e0 = d0 - y0;
+    dot2 = wb0 * e0 + g.sum(dot2);
+    const double ds0 = w_head(e, wb0, dot2, e0);
+    // pass 3: ds and the (s, ds) quadratic
+    double ss = 0.0, d2 = 0.0, sd = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) {
+      const double yt = w_tail(e, 1.0, wbar[o + t], dot1, dz[o + t]);
+      const double dst = w_tail(e, 1.0, wbar[o + t], dot2, d[o + t] - yt);
+      ds[o + t] = dst;
+      const double st = s[o + t];
+      ss += st * st;
+      d2 += dst * dst;
+      sd += st * dst;
+    }
+    ss = g.sum(ss);
+    d2 = g.sum(d2);
+    sd = g.sum(sd);
+    if (g.lane() == 0 && q) {
+      if (wdz) wdz[o] = y0;
+      ds[o] = ds0;
+      acc.viol_s = fmax(acc.viol_s, sqrt(ss) - s0);
+      acc.viol_z = fmax(acc.viol_z, sqrt(zz) - z0);
+      acc.step_s = fmin(acc.step_s, qs_soc_step(ds0 * ds0 - d2, 2.0 * (s0 * ds0 - sd), s0 * s0 - ss));
+      acc.step_z = fmin(acc.step_z, qs_soc_step(dz0 * dz0 - dd, 2.0 * (z0 * dz0 - zd), z0 * z0 - zz));
+    }
+  }
+  __device__ void finish(Acc& a) const {
+    double v[4] = {a.step_s, a.step_z, a.viol_s, a.viol_z};
+    const RedOps<4> ops = {{RED_MIN, RED_MIN, RED_MAX, RED_MAX}};
+    double* sc = scalars;
+    const int corr = corrector;
+    const double sf = step_fraction;
+    qs_grid_reduce<4>(v, ops, gr, [=](double (&t)[4]) {
+      sc[SC_STEP_S] = t[0];
+      sc[SC_STEP_Z] = t[1];
+      sc[SC_VIOL_S] = t[2];
+      sc[SC_VIOL_Z] = t[3];
+      if (!(t[2] < 0.0) || !(t[3] < 0.0)) sc[SC_FLAG_NOT_INTERIOR] = 1.0;
+      if (!corr) {
+        sc[SC_ALPHA_AFF] = fmin(1.0, fmin(t[0], t[1]));
+      } else {
+        const double al = fmin(1.0, sf * fmin(t[0], t[1]));
+        sc[SC_ALPHA] = al;
+        if (!qs_finite(al) || al <= 0.0) sc[SC_FLAG_BAD_STEP] = 1.0;
+      }
+    });
+  }
+};
+
+// -------------------------------------------------- W^T W v = W (W v)  (a-13)
+// Scaling block of the KKT operator, used by the refinement residual.
+struct ApplyW2Op {
+  const double* w;
+  const double* eta;
+  const double* wbar;
+  const double* u;
+  double* out;
+  typedef NoAcc Acc;
+  __device__ void init(Acc&) const {}
+  __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
+    for (int i = tid; i < L.l; i += nth) out[i] = (w[i] * w[i]) * u[i];
+  }
+  template <class Grp>
+  __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
+    const double wb0 = q ? wbar[o] : 0.0, u0 = q ? u[o] : 0.0, e = q ? eta[k] : 1.0;
+    double dot1 = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) dot1 += wbar[o + t] * u[o + t];
+    dot1 = wb0 * u0 + g.sum(dot1);
+    const double y0 = w_head(e, wb0, dot1, u0);
+    double dot2 = 0.0;
+    for (int t = 1 + g.lane(); t < q; t += g.size()) dot2 += wbar[o + t] * w_tail(e, 1.0, wbar[o + t], dot1, u[o + t]);
+    dot2 = wb0 * y0 + g.sum(dot2);
+    for (int t = 1 + g.lane(); t < q; t += g.size())
+      out[o + t] = w_tail(e, 1.0, wbar[o + t], dot2, w_tail(e, 1.0, wbar[o + t], dot1, u[o + t]));
+    if (g.lane() == 0 && q) out[o] = w_head(e, wb0, dot2, y0);
+  }
+  __device__ void finish(Acc&) const {}
+};
+
+// ------------------------------------------------------- plain vector kernels
+__global__ void __launch_bounds__(QS_THREADS) k_mu_aff(int m, const double* s, const double* z, const double* ds,
+                                                       const double* dz, double deg, double* scalars, GridRed gr) {
+  // mu_aff = max(0, (s + a ds).(z + a dz) / deg), mu = s.z / deg,
+  // sigma = clip((mu_aff / mu)^3, 0, 1)                       (ipm.py:198-206)
+  const double a = scalars[SC_ALPHA_AFF];
+  double v[2] = {0.0, 0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const double si = s[i], zi = z[i];
+    v[0] += (si + a * ds[i]) * (zi + a * dz[i]);
+    v[1] += si * zi;
+  }
+  const RedOps<2> ops = {{RED_SUM, RED_SUM}};
+  qs_grid_reduce<2>(v, ops, gr, [=](double (&t)[2]) {
+    const double mu_aff = fmax(0.0, t[0] / deg);
+    const double mu = t[1] / deg;
+    double sigma = 0.0;
+    if (mu > 0.0) {
+      const double r = mu_aff / mu;
+      sigma = fmin(1.0, fmax(0.0, r * r * r));
+    }
+    scalars[SC_MU_AFF] = mu_aff;
+    scalars[SC_MU] = mu;
+    scalars[SC_SIGMA] = sigma;
+  });
+}
+
+__global__ void __launch_bounds__(QS_THREADS) k_update_iterate(int n, int p, int m, double* x, double* y, double* z,
+                                                               double* s, const double* sol, const double* ds,
+                                                               double deg, double* scalars, GridRed gr) {
+  // it' = it + alpha (dx, dy, dz, ds); mu' = s'.z' / deg; finite check (ipm.py:220-234)
+  const double a = scalars[SC_ALPHA];
+  double v[2] = {0.0, 0.0};
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (int i = tid; i < n; i += nth) {
+    const double t = x[i] + a * sol[i];
+    x[i] = t;
+    if (!qs_finite(t)) v[1] = 1.0;
+  }
+  for (int i = tid; i < p; i += nth) {
+    const double t = y[i] + a * sol[n + i];
+    y[i] = t;
+    if (!qs_finite(t)) v[1] = 1.0;
+  }
+  for (int i = tid; i < m; i += nth) {
+    const double zt = z[i] + a * sol[n + p + i];
+    const double st = s[i] + a * ds[i];
+    z[i] = zt;
+    s[i] = st;
+    v[0] += st * zt;
+    if (!qs_finite(zt) || !qs_finite(st)) v[1] = 1.0;
+  }
+  const RedOps<2> ops = {{RED_SUM, RED_MAX}};
+  qs_grid_reduce<2>(v, ops, gr, [=](double (&t)[2]) {
+    scalars[SC_MU] = t[0] / deg;
+    if (t[1] != 0.0 || !qs_finite(t[0])) scalars[SC_FLAG_NONFINITE] = 1.0;
+  });
+}
+
+__global__ void __launch_bounds__(QS_THREADS) k_dot(int m, const double* a, const double* b, double scale, double* out,
+                                                    GridRed gr) {
+  double v[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) v[0] += a[i] * b[i];
+  const RedOps<1> ops = {{RED_SUM}};
+  qs_grid_reduce<1>(v, ops, gr, [=](double (&t)[1]) { *out = t[0] * scale; });
+}
+
+int vec_grid(i64 n) {
+  i64 g = (n + QS_THREADS - 1) / QS_THREADS;
+  if (g < 1) g = 1;
+  if (g > 148 * 8) g = 148 * 8;
+  return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ host launchers
+void qsk_nt_scaling(const ConeLayout& L, const double* s, const double* z, double* w, double* eta, double* wbar,
+                    double* lam, double* lam_sq, double* scalars, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, NtScalingOp{s, z, w, eta, wbar, lam, lam_sq, scalars}, st);
+}
+
+void qsk_apply_w(const ConeLayout& L, const double* w, const double* eta, const double* wbar, const double* u,
+                 double* out, int inverse, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, ApplyWOp{w, eta, wbar, u, out, inverse}, st);
+}
+
+void qsk_apply_w2(const ConeLayout& L, const double* w, const double* eta, const double* wbar, const double* u,
+                  double* out, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, ApplyW2Op{w, eta, wbar, u, out}, st);
+}
+
+void qsk_jordan_product(const ConeLayout& L, const double* u, const double* v, double* out, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, JordanProductOp{u, v, out}, st);
+}
+
+void qsk_jordan_divide(const ConeLayout& L, const double* lam, const double* v, double* out, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, JordanDivideOp{lam, v, out}, st);
+}
+
+void qsk_max_step(const ConeLayout& L, const double* u, const double* du, double* scalars, int slot_step,
+                  int slot_viol, GridRed gr, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, MaxStepOp{u, du, scalars, slot_step, slot_viol, gr}, st);
+}
+
+void qsk_shift(const ConeLayout& L, const double* u, double* out, const double* scalars, int slot, double scale,
+               cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, ShiftOp{u, out, scalars, slot, scale}, st);
+}
+
+void qsk_dcomp(const ConeLayout& L, const double* w, const double* eta, const double* wbar, const double* ds_a,
+               const double* wdz_a, const double* lam_sq, double* dcomp, const double* scalars, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, DcompOp{w, eta, wbar, ds_a, wdz_a, lam_sq, dcomp, scalars}, st);
+}
+
+void qsk_rhs_cone(const ConeLayout& L, const double* w, const double* eta, const double* wbar, const double* lam,
+                  const double* dc, double sign, const double* r_cone, double* d, double* rhs_z, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, RhsConeOp{w, eta, wbar, lam, dc, sign, r_cone, d, rhs_z}, st);
+}
+
+void qsk_post_solve(const ConeLayout& L, const double* w, const double* eta, const double* wbar, const double* d,
+                    const double* dz, const double* s, const double* z, double* wdz, double* ds, double* scalars,
+                    int corrector, double step_fraction, GridRed gr, cudaStream_t st) {
+  if (QS_EMPTY_GUARD(L)) return;
+  launch(L, PostSolveOp{w, eta, wbar, d, dz, s, z, wdz, ds, scalars, corrector, step_fraction, gr}, st);
+}
+
+void qsk_mu_aff(int m, const double* s, const double* z, const double* ds, const double* dz, double deg,
+                double* scalars, GridRed gr, cudaStream_t st) {
+  k_mu_aff<<<vec_grid(m), QS_THREADS, 0, st>>>(m, s, z, ds, dz, deg, scalars, gr);
+}
+
+void qsk_update_iterate(int n, int p, int m, double* x, double* y, double* z, double* s, const double* sol,
+                        const double* ds, double deg, double* scalars, GridRed gr, cudaStream_t st) {
+  i64 big = n > m ? n : m;
+  k_update_iterate<<<vec_grid(big), QS_THREADS, 0, st>>>(n, p, m, x, y, z, s, sol, ds, deg, scalars, gr);
+}
+
+void qsk_dot(int m, const double* a, const double* b, double scale, double* out, GridRed gr, cudaStream_t st) {
+  k_dot<<<vec_grid(m), QS_THREADS, 0, st>>>(m, a, b, scale, out, gr);
+}

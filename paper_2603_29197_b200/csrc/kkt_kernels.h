@@ -1,0 +1,23 @@
+// -W'W generation + scatter into the KKT value array (kkt_kernels.cu).
+#pragma once
+#include "common.cuh"
+
+#define QS_WTW_TILE 8192  // target block entries per CTA
+
+// Built once at setup (host side in capi.cu); all pointers are device pointers.
+struct WtwPlan {
+  int l, nsoc, m;
+  const int* soc_ptr;      // [nsoc+1]
+  const int* cone_of_col;  // [m-l]  cone index of conic column l + c
+  int ntiles;
+  const int* tile_ptr;     // [ntiles+1] global conic column ranges of ~QS_WTW_TILE entries
+  const i64* slot_start;   // [nsoc]  the reference's soc_slot_starts (kkt.py:113-125)
+  const i64* kp_conic;     // [m]  kp_conic[c] = K.col_pointers[n+p+c+1]  (DIRECT mode), may be null
+  double* c4;              // [nsoc] scratch: 4 * sum wbar^2
+  double* e2;              // [nsoc] scratch: eta^2
+};
+
+// mode: 0 dense slots, 1 explicit int64 positions map, 2 closed-form positions
+void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta, const double* wbar,
+                 const i64* positions, double* out, cudaStream_t st);
+void qsk_check_direct_map(const WtwPlan& P, const i64* positions, int* flag, cudaStream_t st);

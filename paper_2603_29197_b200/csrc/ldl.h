@@ -1,0 +1,64 @@
+// GPU supernodal multifrontal LDL' of the quasidefinite KKT matrix.
+//
+// Stands where the paper's cuDSS calls stand (analysis once, numeric
+// refactorisation per iteration, triangular solves): cuDSS is not present in
+// this image, so the factorisation is implemented here.  Semantics follow the
+// reference's LDL (ldl.py:72-122, _kernels.py:102-184): no pivoting, a
+// sign-matched static diagonal shift (+reg on the first n pivots, -reg on the
+// rest) added to the matrix being factorised only, and a dynamic floor
+// |d| < 1e-14 -> +-1e-14 on the pivots.
+//
+// Structure: host symbolic analysis (host_setup.cpp) -> supernodes with dense
+// column-major fronts; numeric phase runs level by level over the supernodal
+// tree (leaves first), one launch per level per phase.  180 GB of HBM lets
+// every front keep its own panel AND update matrix, so there is no stack
+// management and the assembly is a pure gather from the children.
+#pragma once
+#include <string>
+
+#include "common.cuh"
+#include "host_setup.h"
+
+struct DevSym {
+  int nsup;
+  const int* col0;
+  const i64* rowptr;
+  const int* rowidx;
+  const int* childptr;
+  const int* child;
+  const i64* relptr;
+  const int* rel;
+  const i64* Loff;
+  const i64* Uoff;
+  const i64* Boff;
+  const int* sup_of;
+  const int* iperm;
+  const int* perm;
+};
+
+struct LinSys {
+  Symbolic S;
+  DevSym D{};
+  i64 N = 0, knnz = 0;
+  // device storage
+  double* L = nullptr;     // panels
+  double* U = nullptr;     // update matrices
+  double* Dg = nullptr;    // pivots (new numbering)
+  double* B = nullptr;     // solve contribution vectors
+  double* xw = nullptr;    // permuted work vector
+  double* reg = nullptr;   // sign-matched static shift per new column
+  i64* amap = nullptr;     // K entry -> panel storage offset
+  int* d_levelsup = nullptr;
+  std::vector<void*> owned;
+  double dyn_eps = 1e-14;
+  double analysis_seconds = 0.0;
+  size_t device_bytes = 0;
+
+  // Kp/Ki: host pattern (upper CSC); d_Kp/d_Ki: the same on the device.
+  std::string analyze(i64 N, const i64* Kp, const i64* Ki, const i64* d_Kp, const int* d_Ki, int order,
+                      const i64* user_perm, i64 ncliques, const i64* clique_start, const i64* clique_size, i64 n_pos,
+                      double static_reg, cudaStream_t st);
+  void factor(const double* d_Kx, double* scalars, cudaStream_t st);
+  void solve(const double* d_rhs, double* d_sol, cudaStream_t st);  // (L D L')^{-1} rhs, no refinement
+  void release();
+};

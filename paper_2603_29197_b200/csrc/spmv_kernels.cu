@@ -1,0 +1,296 @@
+// Sparse products for the residuals and the refinement operator.
+//
+// The reference keeps P (upper), A and G in CSC and uses a column-scatter
+// product for M x and a column gather-dot for M'x (sparse.py:119-150,
+// _kernels.py:13-43).  A scatter needs atomics on a GPU, so setup builds, once,
+// the row-major views the gathers need:
+//     Pf  = P + P' - diag(P) in CSR      (n x n)
+//     At  = CSC of A read as CSR of A'   (n x p)   -- zero-copy
+//     Gt  = CSC of G read as CSR of G'   (n x m)   -- zero-copy
+//     Ar  = CSR of A                     (p x n)
+//     Gr  = CSR of G                     (m x n)
+// Every product is then a gather-dot with `tpr` (1..32, power of two) lanes
+// per row chosen from the mean row length; sums are deterministic.
+//
+// compute_residuals (ipm.py:70-103) is ONE launch over the row ranges
+// [dual | eq | cone] with all norms reduced in the same pass.
+#include "spmv_kernels.h"
+
+namespace {
+
+__device__ __forceinline__ double row_dot(const Csr& M, int row, const double* __restrict__ x, int lane, int tpr,
+                                          unsigned mask) {
+  double acc = 0.0;
+  if (row < M.rows) {
+    const int e = M.ptr[row + 1];
+    for (int p = M.ptr[row] + lane; p < e; p += tpr) acc += M.val[p] * x[M.idx[p]];
+  }
+  for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
+  return acc;
+}
+
+__device__ __forceinline__ unsigned lane_mask(int tpr) {
+  return tpr == 32 ? 0xffffffffu : (((1u << tpr) - 1u) << (threadIdx.x & 31 & ~(tpr - 1)));
+}
+
+struct RowRange {
+  int which;  // 0 dual, 1 eq, 2 cone
+  int row, stride, lane, tpr;
+  unsigned mask;
+};
+
+// block ranges: nbd blocks stride over the dual rows, nbe over the eq rows, the
+// rest over the cone rows; a group of tpr lanes owns a row
+__device__ __forceinline__ RowRange locate(int nbd, int nbe, int nbc, int tpr_d, int tpr_e, int tpr_c) {
+  RowRange r;
+  int b = blockIdx.x, nb;
+  if (b < nbd) {
+    r.which = 0;
+    r.tpr = tpr_d;
+    nb = nbd;
+  } else if (b < nbd + nbe) {
+    r.which = 1;
+    r.tpr = tpr_e;
+    b -= nbd;
+    nb = nbe;
+  } else {
+    r.which = 2;
+    r.tpr = tpr_c;
+    b -= nbd + nbe;
+    nb = nbc;
+  }
+  r.row = (b * blockDim.x + threadIdx.x) / r.tpr;
+  r.stride = nb * (QS_THREADS / r.tpr);
+  r.lane = threadIdx.x & (r.tpr - 1);
+  r.mask = lane_mask(r.tpr);
+  return r;
+}
+
+__device__ __forceinline__ double absmax(double a, double v) {
+  const double t = fabs(v);
+  return (t > a || t != t) ? t : a;  // NaN sticks
+}
+
+__global__ void __launch_bounds__(QS_THREADS)
+    k_residuals(ResidualArgs A, int nbd, int nbe, int nbc) {
+  enum { PX, ATY, GTZ, RD, XPX, CX, AX, RE, GX, SN, RC, GAP, NV };
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = 0.0;
+  const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
+  if (r.which == 0) {
+    for (int row = r.row; row < A.n; row += r.stride) {
+      const double px = row_dot(A.Pf, row, A.x, r.lane, r.tpr, r.mask);
+      const double aty = row_dot(A.At, row, A.y, r.lane, r.tpr, r.mask);
+      const double gtz = row_dot(A.Gt, row, A.z, r.lane, r.tpr, r.mask);
+      if (r.lane == 0) {
+        const double ci = A.c[row], xi = A.x[row];
+        const double rd = px + ci + aty + gtz;  // ipm.py:76
+        A.rhs[row] = -rd;
+        v[PX] = absmax(v[PX], px);
+        v[ATY] = absmax(v[ATY], aty);
+        v[GTZ] = absmax(v[GTZ], gtz);
+        v[RD] = absmax(v[RD], rd);
+        v[XPX] += xi * px;
+        v[CX] += ci * xi;
+      }
+    }
+  } else if (r.which == 1) {
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double ax = row_dot(A.Ar, row, A.x, r.lane, r.tpr, r.mask);
+      if (r.lane == 0) {
+        const double re = ax - A.b[row];  // ipm.py:77
+        A.rhs[A.n + row] = -re;
+        v[AX] = absmax(v[AX], ax);
+        v[RE] = absmax(v[RE], re);
+      }
+    }
+  } else {
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const double gx = row_dot(A.Gr, row, A.x, r.lane, r.tpr, r.mask);
+      if (r.lane == 0) {
+        const double si = A.s[row];
+        const double rc = gx + si - A.h[row];  // ipm.py:78
+        A.r_cone[row] = rc;
+        v[GX] = absmax(v[GX], gx);
+        v[SN] = absmax(v[SN], si);
+        v[RC] = absmax(v[RC], rc);
+        v[GAP] += si * A.z[row];
+      }
+    }
+  }
+  const RedOps<NV> ops = {{RED_MAX, RED_MAX, RED_MAX, RED_MAX, RED_SUM, RED_SUM, RED_MAX, RED_MAX, RED_MAX, RED_MAX,
+                           RED_MAX, RED_SUM}};
+  double* sc = A.scalars;
+  qs_grid_reduce<NV>(v, ops, A.gr, [=](double (&t)[NV]) {
+    sc[SC_NORM_PX] = t[PX];
+    sc[SC_NORM_ATY] = t[ATY];
+    sc[SC_NORM_GTZ] = t[GTZ];
+    sc[SC_NORM_RDUAL] = t[RD];
+    sc[SC_XPX] = t[XPX];
+    sc[SC_CX] = t[CX];
+    sc[SC_OBJ] = 0.5 * t[XPX] + t[CX];
+    sc[SC_NORM_AX] = t[AX];
+    sc[SC_NORM_REQ] = t[RE];
+    sc[SC_NORM_GX] = t[GX];
+    sc[SC_NORM_S] = t[SN];
+    sc[SC_NORM_RCONE] = t[RC];
+    sc[SC_GAP] = t[GAP];
+    if (!qs_finite(t[RD]) || !qs_finite(t[RE]) || !qs_finite(t[RC]) || !qs_finite(t[GAP]))
+      sc[SC_FLAG_NONFINITE] = 1.0;  // ipm.py:96-102
+  });
+}
+
+// r = rhs - K v with K applied as an operator (blocks P, A, G and W'W):
+//   r_x = rhs_x - (P v_x + A' v_y + G' v_z)
+//   r_y = rhs_y - A v_x
+//   r_z = rhs_z - (G v_x - (W'W v_z))         w2vz precomputed by qsk_apply_w2
+// plus ||r||_inf -> scalars[slot].  Reference: ldl.py:152,159 (there the
+// product runs over the stored entries of K; same operator, other rounding).
+__global__ void __launch_bounds__(QS_THREADS)
+    k_kkt_residual(KktResidualArgs A, int nbd, int nbe, int nbc) {
+  double v[1] = {0.0};
+  const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
+  const double* vx = A.v;
+  const double* vy = A.v + A.n;
+  const double* vz = A.v + A.n + A.p;
+  if (r.which == 0) {
+    for (int row = r.row; row < A.n; row += r.stride) {
+      const double px = row_dot(A.Pf, row, vx, r.lane, r.tpr, r.mask);
+      const double aty = row_dot(A.At, row, vy, r.lane, r.tpr, r.mask);
+      const double gtz = row_dot(A.Gt, row, vz, r.lane, r.tpr, r.mask);
+      if (r.lane == 0) {
+        const double t = A.rhs[row] - (px + aty + gtz);
+        A.r[row] = t;
+        v[0] = absmax(v[0], t);
+      }
+    }
+  } else if (r.which == 1) {
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double ax = row_dot(A.Ar, row, vx, r.lane, r.tpr, r.mask);
+      if (r.lane == 0) {
+        const double t = A.rhs[A.n + row] - ax;
+        A.r[A.n + row] = t;
+        v[0] = absmax(v[0], t);
+      }
+    }
+  } else {
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const double gx = row_dot(A.Gr, row, vx, r.lane, r.tpr, r.mask);
+      if (r.lane == 0) {
+        const int i = A.n + A.p + row;
+        const double t = A.rhs[i] - (gx - A.w2vz[row]);
+        A.r[i] = t;
+        v[0] = absmax(v[0], t);
+      }
+    }
+  }
+  const RedOps<1> ops = {{RED_MAX}};
+  double* out = A.scalars + A.slot;
+  qs_grid_reduce<1>(v, ops, A.gr, [=](double (&t)[1]) { *out = t[0]; });
+}
+
+// plain y (+)= M x, gather form
+__global__ void __launch_bounds__(QS_THREADS) k_spmv_csr(Csr M, const double* x, double* y, int accumulate) {
+  const int tpr = M.tpr;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / tpr;
+  const double d = row_dot(M, row, x, threadIdx.x & (tpr - 1), tpr, lane_mask(tpr));
+  if ((threadIdx.x & (tpr - 1)) == 0 && row < M.rows) y[row] = accumulate ? y[row] + d : d;
+}
+
+// out += sym(M) x for M stored as its upper triangle in CSC -- the reference's
+// literal KKT product (_kernels.py:33-43), kept as the checked alternative to
+// the operator form.  Scatter side uses fp64 atomics (order not fixed).
+__global__ void __launch_bounds__(QS_THREADS)
+    k_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out) {
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (col >= ncols) return;
+  const double xj = x[col];
+  double acc = 0.0;
+  for (i64 p = cp[col] + lane; p < cp[col + 1]; p += 32) {
+    const int i = ri[p];
+    const double v = vx[p];
+    atomicAdd(&out[i], v * xj);
+    if (i != col) acc += v * x[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) atomicAdd(&out[col], acc);
+}
+
+__global__ void __launch_bounds__(QS_THREADS) k_axpby(i64 n, double a, const double* x, double b, const double* y,
+                                                      double* out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + (y ? b * y[i] : 0.0);
+}
+
+__global__ void __launch_bounds__(QS_THREADS) k_absmax(i64 n, const double* x, double* out, double* nonfinite,
+                                                       GridRed gr) {
+  double v[1] = {0.0};
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    v[0] = absmax(v[0], x[i]);
+  const RedOps<1> ops = {{RED_MAX}};
+  qs_grid_reduce<1>(v, ops, gr, [=](double (&t)[1]) {
+    *out = t[0];
+    if (nonfinite && !qs_finite(t[0])) *nonfinite = 1.0;
+  });
+}
+
+int blocks_for(int rows, int tpr) {
+  if (rows <= 0) return 0;
+  const int rpb = QS_THREADS / tpr;
+  return (rows + rpb - 1) / rpb;
+}
+
+int blocks_capped(int rows, int tpr) {
+  const int b = blocks_for(rows, tpr), cap = QS_MAX_GRID / 4;
+  return b > cap ? cap : b;
+}
+
+int vgrid(i64 n) {
+  i64 g = (n + QS_THREADS - 1) / QS_THREADS;
+  if (g < 1) g = 1;
+  if (g > 148 * 8) g = 148 * 8;
+  return (int)g;
+}
+
+}  // namespace
+
+int qsk_pick_tpr(i64 nnz, i64 rows) {
+  if (rows <= 0) return 1;
+  const double mean = (double)nnz / (double)rows;
+  int t = 1;
+  while (t < 32 && t * 2 <= mean) t <<= 1;  // largest power of two <= mean row length
+  return t;
+}
+
+void qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
+  const int nbd = blocks_capped(A.n, A.Pf.tpr), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
+  k_residuals<<<nbd + nbe + nbc, QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
+}
+
+void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st) {
+  const int nbd = blocks_capped(A.n, A.Pf.tpr), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
+  k_kkt_residual<<<nbd + nbe + nbc, QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
+}
+
+void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cudaStream_t st) {
+  if (M.rows <= 0) return;
+  k_spmv_csr<<<blocks_for(M.rows, M.tpr), QS_THREADS, 0, st>>>(M, x, y, accumulate);
+}
+
+void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out,
+                            cudaStream_t st) {
+  if (ncols <= 0) return;
+  const i64 blocks = ((i64)ncols * 32 + QS_THREADS - 1) / QS_THREADS;
+  k_spmv_sym_upper_csc<<<(unsigned)blocks, QS_THREADS, 0, st>>>(ncols, cp, ri, vx, x, out);
+}
+
+void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_axpby<<<vgrid(n), QS_THREADS, 0, st>>>(n, a, x, b, y, out);
+}
+
+void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st) {
+  k_absmax<<<vgrid(n), QS_THREADS, 0, st>>>(n, x, out, nonfinite, gr);
+}

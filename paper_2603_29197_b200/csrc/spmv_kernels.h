@@ -1,0 +1,44 @@
+// Sparse gather products, fused residuals and small vector kernels (spmv_kernels.cu).
+#pragma once
+#include "common.cuh"
+
+struct Csr {
+  int rows, cols;
+  const int* ptr;  // [rows+1]
+  const int* idx;
+  const double* val;
+  int tpr;  // lanes per row (power of two, 1..32)
+};
+
+// compute_residuals (ipm.py:70-103): writes rhs[0:n] = -r_dual, rhs[n:n+p] = -r_eq,
+// r_cone, and every scalar check_termination (ipm.py:106-119) needs.
+struct ResidualArgs {
+  int n, p, m;
+  Csr Pf, At, Gt, Ar, Gr;  // Pf.tpr is used for the whole dual range
+  const double *x, *y, *z, *s, *c, *b, *h;
+  double* rhs;
+  double* r_cone;
+  double* scalars;
+  GridRed gr;
+};
+
+struct KktResidualArgs {
+  int n, p, m;
+  Csr Pf, At, Gt, Ar, Gr;
+  const double* v;     // [n+p+m] candidate solution
+  const double* rhs;   // [n+p+m]
+  const double* w2vz;  // [m]  W'W v_z
+  double* r;           // [n+p+m] out
+  double* scalars;
+  int slot;            // scalars[slot] = ||r||_inf
+  GridRed gr;
+};
+
+int qsk_pick_tpr(i64 nnz, i64 rows);
+void qsk_residuals(const ResidualArgs& A, cudaStream_t st);
+void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st);
+void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cudaStream_t st);
+void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out,
+                            cudaStream_t st);
+void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st);
+void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st);

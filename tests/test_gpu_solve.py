@@ -1,0 +1,147 @@
+"""End-to-end parity of Solver(algebra='cuda') with the reference (golden
+fixtures) and the CPU oracle, plus the backend contract and status paths.
+
+North-star tolerances: iteration count within +-1, objective and residuals to
+a relative 1e-6.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2603_29197_b200 as qs
+from paper_2603_29197_b200.cones import identity_scaling
+from paper_2603_29197_b200.ipm import DeviceSolver, check_termination
+from paper_2603_29197_b200.kkt import assemble_kkt
+from paper_2603_29197_b200.linsys import make_backend
+from paper_2603_29197_b200.problem import Settings, SolveStatus
+from util import golden_problem_names, load_golden, problem_from_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def run(d, **kw):
+    return qs.Solver("cuda").setup(d.n, d.m, d.p, d.P, d.c, d.A, d.b, d.G, d.h, d.cone.orthant_dim,
+                                   len(d.cone.soc_dims), d.cone.soc_dims, **kw).solve()
+
+
+@pytest.mark.parametrize("name", golden_problem_names())
+def test_solve_matches_reference(oracle, name):
+    g = load_golden(name)
+    d = problem_from_golden(g)
+    res = run(d)
+    assert res.status.value == str(g["status"]) == "Solved"
+    assert abs(res.iterations - int(g["iterations"])) <= 1
+    obj = float(g["objective"])
+    assert abs(res.objective - obj) <= 1e-6 * max(1.0, abs(obj))
+    assert res.factor_count == res.iterations + 1 and res.solve_count == 2 * res.iterations + 2  # test_ipm.py:239-243
+    for k in "xyzs":
+        ref = g[k]
+        assert np.max(np.abs(getattr(res, k) - ref), initial=0.0) <= 1e-5 * max(1.0, np.max(np.abs(ref), initial=0.0)), k
+    # the GPU solution satisfies the reference's own termination test when its residuals are recomputed by the oracle
+    it = oracle.Iterate(res.x, res.y, res.z, res.s, 0.0)
+    r = oracle.compute_residuals(oracle.SimpleNamespace(
+        n=d.n, m=d.m, p=d.p, P=oracle._csc(d.P), A=oracle._csc(d.A), G=oracle._csc(d.G), c=d.c, b=d.b, h=d.h,
+        cone=d.cone), it)
+    loose = oracle.OracleSettings(eps_abs=1.000001e-7, eps_rel=1.000001e-7)
+    assert oracle.check_termination(r, it, loose)
+    assert oracle.interior_violation(res.s, d.cone) < 0 and oracle.interior_violation(res.z, d.cone) < 0
+
+
+@pytest.mark.parametrize("name", ["huber_20", "random_0", "tv_denoising_8", "group_lasso_3"])
+def test_initial_iterate_first_residuals_and_first_step(name):
+    g = load_golden(name)
+    d = problem_from_golden(g)
+    dev = DeviceSolver(d, Settings())
+    mu0 = dev.initialize_iterate()
+    it = dev.iterate()
+    for k in "xyzs":
+        ref = g["init_" + k]
+        assert np.allclose(getattr(it, k), ref, rtol=1e-7, atol=1e-7 * np.max(np.abs(ref), initial=1.0)), k
+    assert abs(mu0 - g["trace_mu"][0]) <= 1e-7 * abs(g["trace_mu"][0])
+    r = dev.compute_residuals()
+    gap, obj, nPx, nAty, nGtz, nc, nAx, nb, nGx, nh = g["res0_scalars"]
+    for got, ref in ((r.gap, gap), (r.objective, obj), (r.norm_Px, nPx), (r.norm_Aty, nAty), (r.norm_Gtz, nGtz),
+                     (r.norm_c, nc), (r.norm_Ax, nAx), (r.norm_b, nb), (r.norm_Gx, nGx), (r.norm_h, nh),
+                     (r.norm_r_dual, np.max(np.abs(g["res0_r_dual"]), initial=0.0)),
+                     (r.norm_r_cone, np.max(np.abs(g["res0_r_cone"]), initial=0.0))):
+        assert abs(got - ref) <= 1e-6 * max(1.0, abs(ref))
+    info = dev.ipm_step()
+    alpha, alpha_aff, sigma, mu_aff, mu1 = g["step0_info"]
+    assert abs(info.alpha - alpha) <= 1e-6 and abs(info.alpha_affine - alpha_aff) <= 1e-6
+    assert abs(info.sigma - sigma) <= 1e-5 and abs(info.mu - mu1) <= 1e-6 * max(1.0, abs(mu1))
+    dev.close()
+
+
+def test_backend_contract(oracle):
+    """LinsysBackend lifecycle and numerics (linsys.py:24-108, test_kkt.py:128-168)."""
+    g = load_golden("random_1")
+    d = problem_from_golden(g)
+    kkt = assemble_kkt(d)
+    be = make_backend("cuda")
+    with pytest.raises(RuntimeError):
+        be.factor()
+    be.initialize(kkt, Settings())
+    with pytest.raises(RuntimeError):
+        be.initialize(kkt, Settings())
+    with pytest.raises(RuntimeError):
+        be.solve(np.zeros(kkt.dim))
+    be.update(identity_scaling(d.cone))
+    be.factor()
+    rhs = np.random.default_rng(0).standard_normal(kkt.dim)
+    x = be.solve(rhs)
+    assert (be.n_factor, be.n_solve) == (1, 1)
+    K = kkt.matrix.to_dense_symmetric()
+    assert np.max(np.abs(K @ x - rhs)) <= 1e-9 * (1 + np.max(np.abs(rhs)))
+    # update with a real scaling: device K values equal the oracle's, and the solve follows
+    from util import random_interior_point
+
+    rng = np.random.default_rng(1)
+    sc = oracle.compute_nt_scaling(random_interior_point(d.cone, rng), random_interior_point(d.cone, rng), d.cone)
+    be.update(sc)
+    ref = oracle.assemble_kkt(d)
+    oracle.write_scaling(ref, sc)
+    assert np.allclose(be.kkt_values(), ref.matrix.values, rtol=1e-12, atol=0)
+    be.factor()
+    x = be.solve(rhs)
+    Kd = np.zeros((kkt.dim, kkt.dim))
+    cols = np.repeat(np.arange(kkt.dim), np.diff(ref.matrix.col_pointers))
+    Kd[ref.matrix.row_indices, cols] = ref.matrix.values
+    Kd = Kd + Kd.T - np.diag(np.diag(Kd))
+    assert np.max(np.abs(Kd @ x - rhs)) <= 1e-8 * (1 + np.max(np.abs(rhs)))
+    be.close()
+    with pytest.raises(ValueError):
+        make_backend("builtin")
+
+
+def test_statuses():
+    g = load_golden("huber_20")
+    d = problem_from_golden(g)
+    assert run(d, max_iters=2).status is SolveStatus.MAX_ITERS  # test_ipm.py:245-252
+    assert run(d, time_limit_seconds=1e-9).status is SolveStatus.TIME_LIMIT
+    bad = problem_from_golden(g)
+    bad.c = bad.c.copy()
+    bad.c[0] = np.nan
+    assert run(bad).status is SolveStatus.NUMERICAL_ERROR  # test_ipm.py:290-294
+
+
+def test_orderings_and_literal_refinement_agree():
+    g = load_golden("portfolio_4")
+    d = problem_from_golden(g)
+    a = qs.solve(d, ordering="amd")
+    b = qs.solve(d, ordering="natural")
+    assert a.status is b.status is SolveStatus.SOLVED and abs(a.iterations - b.iterations) <= 1
+    assert abs(a.objective - b.objective) <= 1e-7 * max(1.0, abs(a.objective))
+    dev = DeviceSolver(d, Settings(), kkt_literal=True)
+    st, iters, it = dev.run()
+    dev.close()
+    assert st is SolveStatus.SOLVED and abs(iters - int(g["iterations"])) <= 1
+
+
+def test_deterministic_trace():
+    """Two runs give bitwise-identical iterates (test_ipm.py:217-226): every
+    reduction has a fixed order and there are no atomics on the path."""
+    d = problem_from_golden(load_golden("tv_denoising_8"))
+    a, b = run(d), run(d)
+    for k in "xyzs":
+        assert np.array_equal(getattr(a, k), getattr(b, k))
+    assert a.objective == b.objective and a.iterations == b.iterations
