@@ -1,6 +1,7 @@
 // C ABI of libqsocp_cuda.so (include/qsocp_cuda.h): handle, setup, the
 // per-kernel entry points and the device-resident IPM phases.
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -237,7 +238,7 @@ int solve_refined(qs_handle* h, const double* rhs) {
     h->tm.begin(T_SOLVE, st);
     h->ls.solve(r, out, st);
     h->tm.end(st);
-    h->launches += 3 + 2 * h->ls.S.nlevels;
+    h->launches += h->ls.launches_per_solve();
   };
   auto residual = [&](const double* v, double* r, int slot) {
     h->tm.begin(T_REFINE, st);
@@ -296,7 +297,7 @@ int do_factor(qs_handle* h) {
   h->tm.begin(T_FACTOR, h->stream);
   h->ls.factor(h->d_Kx, h->scalars, h->stream);
   h->tm.end(h->stream);
-  h->launches += 2 + h->ls.S.nlevels;
+  h->launches += h->ls.launches_per_factor();
   h->n_factor++;
   h->factored = true;
   return check_launch(h, "factor");
@@ -492,7 +493,9 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   for (int k : small_ids) mean += (double)q[k];
   mean = small_ids.empty() ? 1.0 : mean / small_ids.size();
   int G = 1;
-  while (G < 32 && G * 4 <= mean) G <<= 1;
+  double div = 4.0;
+  if (const char* e = getenv("QS_GROUP_DIV")) div = atof(e) > 0 ? atof(e) : div;  // tuning knob
+  while (G < 32 && G * div <= mean) G <<= 1;
   L.group = G;
   h->deg = (double)(l + nsoc);
   // -W'W plan: column tiles of ~QS_WTW_TILE block entries
@@ -505,20 +508,27 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   std::vector<i64> slot_start(nsoc);
   i64 slot = l, acc = 0;
   tile_ptr.push_back((int)l);
+  int max_cols = 1, max_window = 1, tile_first_cone_start = (int)l;
+  auto close_tile = [&](int end_col) {
+    max_cols = std::max(max_cols, end_col - tile_ptr.back());
+    max_window = std::max(max_window, end_col - tile_first_cone_start);
+    tile_ptr.push_back(end_col);
+    acc = 0;
+  };
   for (i64 k = 0; k < nsoc; ++k) {
     slot_start[k] = slot;
     slot += q[k] * (q[k] + 1) / 2;
     for (i64 j = 0; j < q[k]; ++j) {
-      const i64 col = ptr[k] + j;
+      const int col = ptr[k] + (int)j;
+      if (col == tile_ptr.back()) tile_first_cone_start = ptr[k];  // first column of a new tile
       cone_of_col[col - l] = (int)k;
       acc += j + 1;
-      if (acc >= QS_WTW_TILE) {
-        tile_ptr.push_back((int)(col + 1));
-        acc = 0;
-      }
+      if (acc >= QS_WTW_TILE || col + 1 - tile_ptr.back() >= QS_WTW_MAXCOLS) close_tile(col + 1);
     }
   }
-  if (tile_ptr.back() != (int)m) tile_ptr.push_back((int)m);
+  if (tile_ptr.back() != (int)m) close_tile((int)m);
+  P.max_tile_cols = max_cols;
+  P.max_tile_window = max_window;
   h->S = slot;
   P.ntiles = (int)tile_ptr.size() - 1;
   P.cone_of_col = h->cone_pool.upload(cone_of_col.data(), cone_of_col.size(), h->stream);

@@ -90,22 +90,85 @@ struct LaneGroup {
     for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mk, v, o);
     return v;
   }
+  // several independent reductions interleaved: same instruction count, the
+  // shuffle latencies overlap instead of adding up
+  __device__ __forceinline__ void sum2(double& a, double& b) const {
+    const unsigned mk = mask();
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double ta = __shfl_xor_sync(mk, a, o), tb = __shfl_xor_sync(mk, b, o);
+      a += ta;
+      b += tb;
+    }
+  }
+  __device__ __forceinline__ void sum3(double& a, double& b, double& c) const {
+    const unsigned mk = mask();
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double ta = __shfl_xor_sync(mk, a, o), tb = __shfl_xor_sync(mk, b, o), tc = __shfl_xor_sync(mk, c, o);
+      a += ta;
+      b += tb;
+      c += tc;
+    }
+  }
+  __device__ __forceinline__ void sum4(double& a, double& b, double& c, double& d) const {
+    const unsigned mk = mask();
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double ta = __shfl_xor_sync(mk, a, o), tb = __shfl_xor_sync(mk, b, o), tc = __shfl_xor_sync(mk, c, o),
+                   td = __shfl_xor_sync(mk, d, o);
+      a += ta;
+      b += tb;
+      c += tc;
+      d += td;
+    }
+  }
 };
 
 struct CtaGroup {
-  double* scratch;  // [32] shared
+  double* scratch;  // [32 * 4] shared
   __device__ __forceinline__ int lane() const { return threadIdx.x; }
   __device__ __forceinline__ int size() const { return blockDim.x; }
-  __device__ __forceinline__ double sum(double v) const {
+  __device__ __forceinline__ void sum4(double& a, double& b, double& c, double& d) const {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();  // scratch may still be read from a previous sum()
-    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ta = __shfl_xor_sync(0xffffffffu, a, o), tb = __shfl_xor_sync(0xffffffffu, b, o),
+                   tc = __shfl_xor_sync(0xffffffffu, c, o), td = __shfl_xor_sync(0xffffffffu, d, o);
+      a += ta;
+      b += tb;
+      c += tc;
+      d += td;
+    }
+    __syncthreads();  // scratch may still be read from a previous reduction
+    if ((threadIdx.x & 31) == 0) {
+      double* sl = scratch + 4 * (threadIdx.x >> 5);
+      sl[0] = a;
+      sl[1] = b;
+      sl[2] = c;
+      sl[3] = d;
+    }
     __syncthreads();
-    double t = 0.0;
+    a = b = c = d = 0.0;
     const int nw = (blockDim.x + 31) >> 5;
-    for (int w = 0; w < nw; ++w) t += scratch[w];
-    return t;
+    for (int w = 0; w < nw; ++w) {
+      a += scratch[4 * w];
+      b += scratch[4 * w + 1];
+      c += scratch[4 * w + 2];
+      d += scratch[4 * w + 3];
+    }
+  }
+  __device__ __forceinline__ double sum(double v) const {
+    double b = 0.0, c = 0.0, d = 0.0;
+    sum4(v, b, c, d);
+    return v;
+  }
+  __device__ __forceinline__ void sum2(double& a, double& b) const {
+    double c = 0.0, d = 0.0;
+    sum4(a, b, c, d);
+  }
+  __device__ __forceinline__ void sum3(double& a, double& b, double& c) const {
+    double d = 0.0;
+    sum4(a, b, c, d);
   }
 };
 

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(QS_THREADS) cone_kernel(ConeLayout L, Op op, i
       op.soc(acc, g, k, o, L.soc_ptr[k + 1] - o);
     }
   } else {
-    __shared__ double scratch[32];
+    __shared__ double scratch[128];
     CtaGroup g{scratch};
     for (int id = b - nb_orth - nb_small; id < L.nbig; id += nb_big) {
       const int k = L.big_ids[id];
@@ -139,9 +139,7 @@ struct NtScalingOp {
       zz += b1 * b1;
       sz += a1 * b1;
     }
-    ss = g.sum(ss);
-    zz = g.sum(zz);
-    sz = g.sum(sz);
+    g.sum3(ss, zz, sz);
     const double sres = s0 * s0 - ss, zres = z0 * z0 - zz;
     // a cone that is not strictly interior raises the flag and writes nothing
     // (the reference aborts with NotInterior, cones.py:182-183)
@@ -154,10 +152,14 @@ struct NtScalingOp {
     const double den = sqrt(2.0 * (1.0 + nt0));
     const double wb0 = (nt0 + 1.0) / den;
     const double ek = sqrt(sa / za);
+    // per-cone reciprocals: the tail of wbar is (s_t/sa - z_t/za) / (2 gamma) / den in the reference
+    // (_cone_kernels.py:43-44); multiplying by 1/sa, 1/za, 1/(2 gamma den) moves each entry by <= 2 ulp
+    // and takes four fp64 divisions per element off the critical path
+    const double isa = 1.0 / sa, iza = 1.0 / za, ik = 1.0 / ((2.0 * gamma) * den);
     double wz = 0.0;
     for (int t = 1 + g.lane(); t < q; t += g.size()) {
       const double zt = z[o + t];
-      const double wbt = (s[o + t] / sa - zt / za) / (2.0 * gamma) / den;
+      const double wbt = (s[o + t] * isa - zt * iza) * ik;
       wbar[o + t] = wbt;
       wz += wbt * zt;
     }
@@ -166,7 +168,7 @@ struct NtScalingOp {
     double ll = 0.0;
     for (int t = 1 + g.lane(); t < q; t += g.size()) {
       const double zt = z[o + t];
-      const double wbt = (s[o + t] / sa - zt / za) / (2.0 * gamma) / den;
+      const double wbt = (s[o + t] * isa - zt * iza) * ik;
       const double lt = ek * (2.0 * wbt * wz + zt);
       lam[o + t] = lt;
       ll += lt * lt;
@@ -260,8 +262,7 @@ struct JordanDivideOp {
       ll += lt * lt;
       cross += lt * v[o + t];
     }
-    ll = g.sum(ll);
-    cross = g.sum(cross);
+    g.sum2(ll, cross);
     const double u0 = (a * v0 - cross) / (a * a - ll);
     for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = (v[o + t] - u0 * lam[o + t]) / a;
     if (g.lane() == 0 && q) out[o] = u0;
@@ -308,11 +309,7 @@ struct MaxStepOp {
         ud += ut * dt;
       }
     }
-    uu = g.sum(uu);
-    if (du) {
-      dd = g.sum(dd);
-      ud = g.sum(ud);
-    }
+    g.sum3(uu, dd, ud);
     if (q && g.lane() == 0) {
       const double u0 = u[o];
       acc.viol = fmax(acc.viol, sqrt(uu) - u0);
@@ -440,20 +437,20 @@ struct RhsConeOp {
       ll += lt * lt;
       cross += lt * (sign * dc[o + t]);
     }
-    ll = g.sum(ll);
-    cross = g.sum(cross);
+    g.sum2(ll, cross);
     const double d0 = (a * v0 - cross) / (a * a - ll);
+    const double ia = 1.0 / a;
     const double wb0 = q ? wbar[o] : 0.0;
     double dot = 0.0;
     for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) / a;
+      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) * ia;
       d[o + t] = dt;
       dot += wbar[o + t] * dt;
     }
     dot = wb0 * d0 + g.sum(dot);
     const double e = q ? eta[k] : 1.0;
     for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) / a;
+      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) * ia;
       rhs_z[o + t] = -r_cone[o + t] - w_tail(e, 1.0, wbar[o + t], dot, dt);
     }
     if (g.lane() == 0 && q) {
@@ -517,10 +514,8 @@ struct PostSolveOp {
       dd += dzt * dzt;
       zd += zt * dzt;
     }
-    dot1 = wb0 * dz0 + g.sum(dot1);
-    zz = g.sum(zz);
-    dd = g.sum(dd);
-    zd = g.sum(zd);
+    g.sum4(dot1, zz, dd, zd);
+    dot1 = wb0 * dz0 + dot1;
     const double y0 = w_head(e, wb0, dot1, dz0);
     // pass 2: w.(d - wdz)
     double dot2 = 0.0;
@@ -543,9 +538,7 @@ struct PostSolveOp {
       d2 += dst * dst;
       sd += st * dst;
     }
-    ss = g.sum(ss);
-    d2 = g.sum(d2);
-    sd = g.sum(sd);
+    g.sum3(ss, d2, sd);
     if (g.lane() == 0 && q) {
       if (wdz) wdz[o] = y0;
       ds[o] = ds0;

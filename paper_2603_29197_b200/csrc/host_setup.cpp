@@ -5,6 +5,14 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
+static double hs_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static bool hs_verbose() { return getenv("QS_VERBOSE") != nullptr; }
 
 // ------------------------------------------------------------------ transpose
 void hs_transpose(i64 rows, i64 cols, const i64* p, const i64* idx, const double* x, i64* tp, i64* ti, double* tx) {
@@ -158,8 +166,8 @@ void build_graph(i64 N, const i64* Kp, const i64* Ki, const int* clique_of, Grap
 // ------------------------------------------------------------------------ AMD
 // Approximate minimum degree on a quotient graph (variables + elements), after
 // Amestoy, Davis & Duff.  Cliques of the input (the dense SOC blocks of the KKT
-// matrix) enter as initial ELEMENTS, so a q x q block costs q list entries
-// instead of q^2/2.  Features: approximate external degrees, element
+// matrix) enter as pre-merged weighted supervariables, so a q x q block costs one
+// node instead of q^2/2 edges.  Features: approximate external degrees, element
 // absorption (incl. aggressive), mass elimination, supervariable detection by
 // hashing, dense-row deferral.
 namespace {
@@ -197,49 +205,48 @@ struct Amd {
 
 }  // namespace
 
-static void amd_core(i64 N, const Graph& g, const std::vector<std::pair<int, int>>& cliques, std::vector<int>* perm_out) {
+// N nodes with positive integer weights (a weight-w node stands for w original
+// variables that are eliminated together); perm_out lists the nodes in
+// elimination order.
+static void amd_core(i64 N, const Graph& g, const std::vector<int>& weight, std::vector<int>* perm_out) {
   Amd a;
   a.N = N;
-  const int nc = (int)cliques.size();
-  a.NT = (int)N + nc;
+  a.NT = (int)N;
+  i64 W = 0;
+  for (i64 v = 0; v < N; ++v) W += weight[v];
   a.adj.resize(N);
   a.elems.resize(N);
   a.Le.resize(a.NT);
-  a.nv.assign(N, 1);
+  a.nv = weight;
   a.degree.assign(N, 0);
   a.elem_deg.assign(a.NT, 0);
   a.absorbed_into.assign(N, -1);
   a.elem_alive.assign(a.NT, 0);
   a.w.assign(a.NT, 0);
-  a.head.assign(N + 1, -1);
+  a.head.assign(W + 1, -1);
   a.next.assign(N, -1);
   a.prev.assign(N, -1);
-  for (i64 v = 0; v < N; ++v) a.adj[v].assign(g.adj.begin() + g.ptr[v], g.adj.begin() + g.ptr[v + 1]);
-  for (int c = 0; c < nc; ++c) {
-    const int e = (int)N + c;
-    a.Le[e].resize(cliques[c].second);
-    std::iota(a.Le[e].begin(), a.Le[e].end(), cliques[c].first);
-    a.elem_alive[e] = 1;
-    a.elem_deg[e] = cliques[c].second;
-    for (int v : a.Le[e]) a.elems[v].push_back(e);
-  }
   for (i64 v = 0; v < N; ++v) {
-    i64 dgr = (i64)a.adj[v].size();
-    for (int e : a.elems[v]) dgr += a.elem_deg[e] - 1;
-    a.degree[v] = (int)std::min<i64>(dgr, N - 1);
+    a.adj[v].assign(g.adj.begin() + g.ptr[v], g.adj.begin() + g.ptr[v + 1]);
+    i64 dgr = 0;
+    for (int u : a.adj[v]) dgr += weight[u];
+    a.degree[v] = (int)std::min<i64>(dgr, W - 1);
   }
   // dense rows/columns are ordered last
-  const i64 dense = std::max<i64>(16, (i64)(10.0 * std::sqrt((double)N)));
+  const i64 dense = std::max<i64>(16, (i64)(10.0 * std::sqrt((double)W)));
   std::vector<int> dense_nodes;
   i64 nel = 0;
+  i64 dense_weight = 0;
   for (i64 v = 0; v < N; ++v) {
-    if (a.degree[v] > dense) {
+    if (a.nv[v] > 0 && a.degree[v] > dense) {
       dense_nodes.push_back((int)v);
+      dense_weight += a.nv[v];
       a.nv[v] = 0;
-      nel++;
+      a.absorbed_into[v] = -1;
     }
   }
-  a.mindeg = (int)N;
+  nel = dense_weight;
+  a.mindeg = (int)W;
   for (i64 v = 0; v < N; ++v)
     if (a.nv[v] > 0) a.list_insert((int)v);
 
@@ -247,11 +254,11 @@ static void amd_core(i64 N, const Graph& g, const std::vector<std::pair<int, int
   pivots.reserve(N);
   std::vector<int> Lme, hashes(N, 0), stamp(a.NT, 0), bucket_head, bucket_next(N, -1);
   int stampv = 0;
-  const i64 nprincipal_total = N - (i64)dense_nodes.size();
+  const i64 nprincipal_total = W - dense_weight;
   i64 eliminated = 0;
 
   while (eliminated < nprincipal_total) {
-    while (a.mindeg <= N && a.head[a.mindeg] < 0) a.mindeg++;
+    while (a.mindeg <= W && a.head[a.mindeg] < 0) a.mindeg++;
     const int me = a.head[a.mindeg];
     a.list_remove(me);
     int nvpiv = a.nv[me];
@@ -337,7 +344,7 @@ static void amd_core(i64 N, const Graph& g, const std::vector<std::pair<int, int
         hashes[i] = (int)(hash % 1000003u);
       }
     }
-    a.wflg += (i64)N + 2;
+    a.wflg += W + 2;
     // supervariable detection among the survivors of Lme
     {
       std::vector<int> live;
@@ -390,7 +397,7 @@ static void amd_core(i64 N, const Graph& g, const std::vector<std::pair<int, int
     nel += nvpiv;
     eliminated += nvpiv;
     size_t kl = 0;
-    const i64 nleft = N - nel;
+    const i64 nleft = W - nel;
     for (int i : Lme) {
       if (a.nv[i] >= 0) continue;  // absorbed
       const int nvi = -a.nv[i];
@@ -434,7 +441,87 @@ static void amd_core(i64 N, const Graph& g, const std::vector<std::pair<int, int
 void amd_order(i64 N, const i64* Kp, const i64* Ki, std::vector<int>* perm) {
   Graph g;
   build_graph(N, Kp, Ki, nullptr, &g);
-  amd_core(N, g, {}, perm);
+  amd_core(N, g, std::vector<int>(N, 1), perm);
+}
+
+// Cone-block AMD for conic KKT patterns.  Every dense SOC block is a clique; a
+// variable whose only clique neighbours lie in ONE block (in the KKT matrix: an x
+// column touching a single second-order cone, e.g. the group variables and the
+// epigraph variable of a group-lasso cone) is "private" to it.  Block = clique +
+// its private variables.  Blocks are eliminated as units: AMD runs on the
+// compressed graph (blocks as weighted nodes), then each block expands to
+// [private variables, clique rows].  One pivot per cone instead of one per row.
+static void block_amd(i64 N, const Graph& g, const std::vector<std::pair<int, int>>& cliques, const int* clique_of,
+                      std::vector<int>* perm) {
+  const int nb = (int)cliques.size();
+  std::vector<int> comp(N, -1);
+  for (int c = 0; c < nb; ++c)
+    for (int t = 0; t < cliques[c].second; ++t) comp[cliques[c].first + t] = c;
+  std::vector<std::vector<int>> priv(nb);
+  for (i64 v = 0; v < N; ++v) {
+    if (clique_of[v] >= 0) continue;
+    int owner = -1;
+    for (i64 k = g.ptr[v]; k < g.ptr[v + 1]; ++k) {
+      const int c = clique_of[g.adj[k]];
+      if (c < 0) continue;
+      if (owner == -1)
+        owner = c;
+      else if (owner != c) {
+        owner = -2;
+        break;
+      }
+    }
+    if (owner >= 0) {
+      comp[v] = owner;
+      priv[owner].push_back((int)v);
+    }
+  }
+  int Nc = nb;
+  std::vector<int> single;  // compressed id - nb -> original node
+  for (i64 v = 0; v < N; ++v)
+    if (comp[v] < 0) {
+      comp[v] = Nc++;
+      single.push_back((int)v);
+    }
+  std::vector<int> weight(Nc, 1);
+  for (int c = 0; c < nb; ++c) weight[c] = cliques[c].second + (int)priv[c].size();
+  // compressed adjacency, deduplicated
+  Graph gc;
+  gc.ptr.assign(Nc + 1, 0);
+  std::vector<std::vector<int>> cadj(Nc);
+  {
+    std::vector<int> seen(Nc, -1);
+    auto gather = [&](int cn, int v) {
+      for (i64 k = g.ptr[v]; k < g.ptr[v + 1]; ++k) {
+        const int u = comp[g.adj[k]];
+        if (u != cn && seen[u] != cn) {
+          seen[u] = cn;
+          cadj[cn].push_back(u);
+        }
+      }
+    };
+    for (int c = 0; c < nb; ++c) {
+      for (int t = 0; t < cliques[c].second; ++t) gather(c, cliques[c].first + t);
+      for (int v : priv[c]) gather(c, v);
+    }
+    for (size_t k = 0; k < single.size(); ++k) gather(nb + (int)k, single[k]);
+  }
+  for (int v = 0; v < Nc; ++v) gc.ptr[v + 1] = gc.ptr[v] + (i64)cadj[v].size();
+  gc.adj.resize(gc.ptr[Nc]);
+  for (int v = 0; v < Nc; ++v) std::copy(cadj[v].begin(), cadj[v].end(), gc.adj.begin() + gc.ptr[v]);
+  std::vector<std::vector<int>>().swap(cadj);
+  std::vector<int> order;
+  amd_core(Nc, gc, weight, &order);
+  perm->clear();
+  perm->reserve(N);
+  for (int cn : order) {
+    if (cn < nb) {
+      for (int v : priv[cn]) perm->push_back(v);
+      for (int t = 0; t < cliques[cn].second; ++t) perm->push_back(cliques[cn].first + t);
+    } else {
+      perm->push_back(single[cn - nb]);
+    }
+  }
 }
 
 // ------------------------------------------------------------------- symbolic
@@ -601,11 +688,19 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   const int* cof = clique_of.empty() ? nullptr : clique_of.data();
 
   // 1. fill-reducing order
+  double t_mark = hs_now();
+  auto lap = [&](const char* what) {
+    if (hs_verbose()) fprintf(stderr, "[qs symbolic] %-28s %8.3f s\n", what, hs_now() - t_mark);
+    t_mark = hs_now();
+  };
   std::vector<int> perm(N);
   if (order == 1) {
     Graph g;
     build_graph(N, Kp, Ki, cof, &g);
-    amd_core(N, g, cliques, &perm);
+    if (cliques.empty())
+      amd_core(N, g, std::vector<int>(N, 1), &perm);
+    else
+      block_amd(N, g, cliques, cof, &perm);
   } else if (order == 2 && user_perm) {
     std::vector<char> seen(N, 0);
     for (i64 k = 0; k < N; ++k) {
@@ -616,6 +711,7 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   } else {
     std::iota(perm.begin(), perm.end(), 0);
   }
+  lap("ordering");
   if ((i64)perm.size() != N) return "ordering produced a wrong-sized permutation";
   std::vector<int> iperm(N);
   for (i64 k = 0; k < N; ++k) iperm[perm[k]] = (int)k;
@@ -637,17 +733,45 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   for (i64 j = 0; j < N; ++j)
     if (parent[j] != -1 && parent[j] <= j) return "internal: tree is not postordered";
 
+  lap("etree + postorder");
   // 3. column counts and supernodes (maximal chains with nested structure)
   std::vector<int> cc;
   column_counts(N, B, parent, &cc);
+  lap("column counts");
   std::vector<int> nchild(N, 0);
   for (i64 j = 0; j < N; ++j)
     if (parent[j] >= 0) nchild[parent[j]]++;
   S->col0.clear();
   S->sup_of.assign(N, 0);
+  // Fundamental chains (parent[j-1] == j with nested structure) merge for free.
+  // Relaxed amalgamation on top: a chain child whose columns directly precede its
+  // parent's is merged while the explicit zeros this pads into the merged panel stay
+  // below QS_RELAX (default 0.4) of the panel.  This turns the row-by-row chain of a
+  // cone block (each row adds a few new rows of structure) into one dense front.
+  double relax = 0.4;
+  if (const char* e = getenv("QS_RELAX")) relax = atof(e);
+  i64 g_ns = 0, g_nr = 0, g_zeros = 0;  // current group: columns, front rows, padded zeros
   for (i64 j = 0; j < N; ++j) {
-    const bool chain = j > 0 && parent[j - 1] == j && cc[j - 1] == cc[j] + 1;
-    if (!chain) S->col0.push_back((int)j);
+    bool merge = false;
+    if (j > 0 && parent[j - 1] == j) {
+      // merged front: g_ns + 1 columns, rows = g_ns + cc[j]
+      const i64 nr_new = g_ns + cc[j];
+      const i64 add = g_ns * (nr_new - g_nr);  // previous columns padded to the new height
+      const i64 zeros = g_zeros + add;
+      const double panel = (double)(g_ns + 1) * (double)nr_new;
+      if (add == 0 || (double)zeros <= relax * panel) {
+        merge = true;
+        g_zeros = zeros;
+        g_nr = nr_new;
+        g_ns += 1;
+      }
+    }
+    if (!merge) {
+      S->col0.push_back((int)j);
+      g_ns = 1;
+      g_nr = cc[j];
+      g_zeros = 0;
+    }
     S->sup_of[j] = (int)S->col0.size() - 1;
   }
   S->nsup = (int)S->col0.size();
@@ -673,8 +797,8 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
 
   // 5. front row structures, bottom-up (children precede parents)
   S->rowptr.assign(nsup + 1, 0);
-  for (int s = 0; s < nsup; ++s) S->rowptr[s + 1] = S->rowptr[s] + cc[S->col0[s]];
-  S->rowidx.resize(S->rowptr[nsup]);
+  S->rowidx.clear();
+  S->rowidx.reserve((size_t)N * 4);
   {
     // lower pattern by column again (rows > col), from B
     std::vector<i64> lp(N + 1, 0);
@@ -688,19 +812,15 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
     std::vector<int> mark(N, -1);
     for (int s = 0; s < nsup; ++s) {
       const int c0 = S->col0[s], c1 = S->col0[s + 1];
-      int* rows = S->rowidx.data() + S->rowptr[s];
-      const i64 cap = S->rowptr[s + 1] - S->rowptr[s];
-      i64 cnt = 0;
+      const size_t begin = S->rowidx.size();
       for (int c = c0; c < c1; ++c) {
         mark[c] = s;
-        if (cnt < cap) rows[cnt] = c;
-        cnt++;
+        S->rowidx.push_back(c);
       }
       auto add = [&](int r) {
         if (r >= c1 && mark[r] != s) {
           mark[r] = s;
-          if (cnt < cap) rows[cnt] = r;
-          cnt++;
+          S->rowidx.push_back(r);
         }
       };
       for (int c = c0; c < c1; ++c)
@@ -710,11 +830,12 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
         const int nsc = S->col0[ch + 1] - S->col0[ch];
         for (i64 k = S->rowptr[ch] + nsc; k < S->rowptr[ch + 1]; ++k) add(S->rowidx[k]);
       }
-      if (cnt != cap) return "internal: front size disagrees with the column count";
-      std::sort(rows + (c1 - c0), rows + cnt);
+      std::sort(S->rowidx.begin() + begin + (c1 - c0), S->rowidx.end());
+      S->rowptr[s + 1] = (i64)S->rowidx.size();
+      if ((i64)(S->rowidx.size() - begin) < cc[c0]) return "internal: front smaller than its first column count";
     }
   }
-
+  lap("front structures");
   // 6. relative indices, storage offsets, levels, statistics
   S->relptr.assign(nsup + 1, 0);
   S->Loff.assign(nsup + 1, 0);
@@ -771,5 +892,6 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   }
   S->perm.swap(perm);
   S->iperm.swap(iperm);
+  lap("rel indices + levels");
   return std::string();
 }

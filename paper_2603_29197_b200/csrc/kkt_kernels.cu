@@ -41,12 +41,25 @@ __global__ void __launch_bounds__(QS_THREADS) k_wtw_prepass(int nsoc, const int*
   }
 }
 
+// Per-column constants staged once per tile.  With A = -eta^2 (4c+4) w_j every
+// tail-tail entry is A*w_i; row 0 uses A0 = -eta^2 4c w_j, the (0,0) entry
+// -eta^2((4c-4) w_0^2 + 1), the diagonal adds -eta^2.  Algebraically identical
+// to _cone_kernels.py:176-185 (the +-2 w_i w_j terms cancel or double); it
+// differs from the reference's expression by rounding only (<= a few ulp).
+struct ColMeta {
+  double A, A0, ne2;
+  i64 base;  // destination of row 0 of this column
+  int j;     // local column index inside its cone
+  int woff;  // offset of the cone's wbar inside the staged window
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(QS_THREADS)
-    k_neg_wtw(int l, int nb_orth, const double* __restrict__ w, const double* __restrict__ wbar,
-              const int* __restrict__ soc_ptr, const int* __restrict__ cone_of_col, const int* __restrict__ tile_ptr,
-              const double* __restrict__ c4, const double* __restrict__ e2, const i64* __restrict__ slot_start,
-              const i64* __restrict__ positions, const i64* __restrict__ kp_conic, double* __restrict__ out) {
+    k_neg_wtw(int l, int nb_orth, int max_cols, int wcap, const double* __restrict__ w,
+              const double* __restrict__ wbar, const int* __restrict__ soc_ptr, const int* __restrict__ cone_of_col,
+              const int* __restrict__ tile_ptr, const double* __restrict__ c4, const double* __restrict__ e2,
+              const i64* __restrict__ slot_start, const i64* __restrict__ positions,
+              const i64* __restrict__ kp_conic, double* __restrict__ out) {
   if ((int)blockIdx.x < nb_orth) {
     // orthant diagonal: slot i holds -(w_i^2)                    (cones.py:324-326)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l; i += nb_orth * blockDim.x) {
@@ -57,33 +70,69 @@ __global__ void __launch_bounds__(QS_THREADS)
     }
     return;
   }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ColMeta* meta = reinterpret_cast<ColMeta*>(smem_raw);
+  double* wst = reinterpret_cast<double*>(smem_raw + (size_t)max_cols * sizeof(ColMeta));
   const int tile = blockIdx.x - nb_orth;
   const int col0 = tile_ptr[tile], col1 = tile_ptr[tile + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  for (int col = col0 + warp; col < col1; col += nwarp) {
+  const int ncols = col1 - col0;
+  // window of wbar covering every cone touched by the tile: [wlo, col1)
+  const int wlo = soc_ptr[cone_of_col[col0 - l]];
+  const int wlen = col1 - wlo;
+  const bool staged = wlen <= wcap;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    const int col = col0 + c;
     const int k = cone_of_col[col - l];
     const int o = soc_ptr[k];
     const int j = col - o;
-    const double cc = c4[k], ne2 = -e2[k];
-    const double wj = wbar[col];
-    const double jj = (j == 0) ? wj : -wj;
-    i64 base;
-    if (MODE == MODE_DIRECT) {
-      base = kp_conic[col] - (j + 1);
+    const double cc = c4[k], ne2 = -e2[k], wj = wbar[col];
+    ColMeta m;
+    m.ne2 = ne2;
+    m.j = j;
+    m.woff = o - wlo;
+    if (j == 0) {
+      m.A = 0.0;
+      m.A0 = ne2 * ((cc - 4.0) * wj);  // times w_0 below, then the diagonal term
     } else {
-      base = slot_start[k] + (i64)j * (j + 1) / 2;
+      m.A = ne2 * ((cc + 4.0) * wj);
+      m.A0 = ne2 * (cc * wj);
     }
-    for (int i = lane; i <= j; i += 32) {
-      const double wi = wbar[o + i];
-      const double ji = (i == 0) ? wi : -wi;
-      // 4 c wi wj - 2 wi (Jw)_j - 2 (Jw)_i wj (+1 on the diagonal), times -eta^2
-      double v = cc * wi * wj - 2.0 * wi * jj - 2.0 * ji * wj;
-      if (i == j) v += 1.0;
-      v = ne2 * v;
-      if (MODE == MODE_MAP) {
-        out[positions[base + i]] = v;
-      } else {
-        out[base + i] = v;
+    m.base = (MODE == MODE_DIRECT) ? kp_conic[col] - (j + 1) : slot_start[k] + (i64)j * (j + 1) / 2;
+    meta[c] = m;
+  }
+  if (staged)
+    for (int t = threadIdx.x; t < wlen; t += blockDim.x) wst[t] = wbar[wlo + t];
+  __syncthreads();
+  // streaming phase: a warp owns a contiguous chunk of the tile's columns; the
+  // interior of a column (0 < i < j) is a pure multiply-store stream, the two
+  // special entries (row 0, diagonal) are written by one lane each.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  const int per = (ncols + nwarp - 1) / nwarp;
+  const int cbeg = warp * per, cend = min(ncols, cbeg + per);
+  for (int c = cbeg; c < cend; ++c) {
+    const double A = meta[c].A;
+    const int j = meta[c].j;
+    const i64 base = meta[c].base;
+    const double* wc = (staged ? wst : wbar + wlo) + meta[c].woff;
+    if (MODE == MODE_MAP) {
+      const i64* pmap = positions + base;
+#pragma unroll 2
+      for (int i = 1 + lane; i < j; i += 32) out[pmap[i]] = A * wc[i];
+      if (lane == 0) {
+        const double v0 = meta[c].A0 * wc[0];
+        out[pmap[0]] = (j == 0) ? v0 + meta[c].ne2 : v0;
+      } else if (lane == 1 && j > 0) {
+        out[pmap[j]] = A * wc[j] + meta[c].ne2;
+      }
+    } else {
+      double* dst = out + base;
+#pragma unroll 2
+      for (int i = 1 + lane; i < j; i += 32) dst[i] = A * wc[i];
+      if (lane == 0) {
+        const double v0 = meta[c].A0 * wc[0];
+        dst[0] = (j == 0) ? v0 + meta[c].ne2 : v0;
+      } else if (lane == 1 && j > 0) {
+        dst[j] = A * wc[j] + meta[c].ne2;
       }
     }
   }
@@ -127,15 +176,23 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
   const int nb_orth = orth_blocks(P.l);
   const int grid = nb_orth + P.ntiles;
   if (grid == 0) return;
+  const int wcap = P.max_tile_window < QS_WTW_WCAP ? P.max_tile_window : QS_WTW_WCAP;
+  const size_t smem = (size_t)P.max_tile_cols * sizeof(ColMeta) + (size_t)wcap * sizeof(double);
+  static bool attr_set[3] = {false, false, false};
+  auto launch = [&](auto kern, int idx, const i64* pos, const i64* kpc) {
+    if (smem > 48 * 1024 && !attr_set[idx]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set[idx] = true;
+    }
+    kern<<<grid, QS_THREADS, smem, st>>>(P.l, nb_orth, P.max_tile_cols, wcap, w, wbar, P.soc_ptr, P.cone_of_col,
+                                         P.tile_ptr, P.c4, P.e2, P.slot_start, pos, kpc, out);
+  };
   if (mode == MODE_SLOTS)
-    k_neg_wtw<MODE_SLOTS><<<grid, QS_THREADS, 0, st>>>(P.l, nb_orth, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,
-                                                        P.c4, P.e2, P.slot_start, nullptr, nullptr, out);
+    launch(k_neg_wtw<MODE_SLOTS>, 0, nullptr, nullptr);
   else if (mode == MODE_MAP)
-    k_neg_wtw<MODE_MAP><<<grid, QS_THREADS, 0, st>>>(P.l, nb_orth, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,
-                                                      P.c4, P.e2, P.slot_start, positions, nullptr, out);
+    launch(k_neg_wtw<MODE_MAP>, 1, positions, nullptr);
   else
-    k_neg_wtw<MODE_DIRECT><<<grid, QS_THREADS, 0, st>>>(P.l, nb_orth, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,
-                                                         P.c4, P.e2, nullptr, nullptr, P.kp_conic, out);
+    launch(k_neg_wtw<MODE_DIRECT>, 2, nullptr, P.kp_conic);
 }
 
 void qsk_check_direct_map(const WtwPlan& P, const i64* positions, int* flag, cudaStream_t st) {

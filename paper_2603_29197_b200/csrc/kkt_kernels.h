@@ -2,7 +2,9 @@
 #pragma once
 #include "common.cuh"
 
-#define QS_WTW_TILE 8192  // target block entries per CTA
+#define QS_WTW_TILE 8192       // target block entries per CTA
+#define QS_WTW_MAXCOLS 512     // at most this many columns per tile (metadata lives in shared memory)
+#define QS_WTW_WCAP 8192       // wbar window staged in shared memory when it fits (doubles)
 
 // Built once at setup (host side in capi.cu); all pointers are device pointers.
 struct WtwPlan {
@@ -11,6 +13,8 @@ struct WtwPlan {
   const int* cone_of_col;  // [m-l]  cone index of conic column l + c
   int ntiles;
   const int* tile_ptr;     // [ntiles+1] global conic column ranges of ~QS_WTW_TILE entries
+  int max_tile_cols;       // widest tile (columns)
+  int max_tile_window;     // longest wbar window [first cone start, tile end) over the tiles
   const i64* slot_start;   // [nsoc]  the reference's soc_slot_starts (kkt.py:113-125)
   const i64* kp_conic;     // [m]  kp_conic[c] = K.col_pointers[n+p+c+1]  (DIRECT mode), may be null
   double* c4;              // [nsoc] scratch: 4 * sum wbar^2

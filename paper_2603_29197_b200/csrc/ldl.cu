@@ -72,9 +72,113 @@ __global__ void __launch_bounds__(LDL_THREADS) k_add_reg(int N, DevSym S, const 
   }
 }
 
-// One CTA per front of the level: gather the children's update matrices
-// (extend-add, fixed child order -> deterministic), factor the pivot panel,
-// form this front's own update matrix.
+// Extend-add (assembly of the children's update matrices into a front), one
+// launch per level.  A CTA owns a slab of 8 consecutive front columns of one
+// front; warp w owns column c_lo + w outright and walks the children in their
+// fixed order, so every front entry is summed by one warp in a fixed order:
+// deterministic, no atomics.  The search "does child c have a column that maps
+// to mine?" runs 32 children at a time (one per lane, binary search in the
+// sorted relative-index list); hits are then processed one by one with the
+// whole warp striding over the child's rows.
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_extend_add(DevSym S, const SlabItem* items, double* L, double* U) {
+  const SlabItem it = items[blockIdx.x];
+  const int s = it.front;
+  const Front f = front_of(S, s, L, U);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pc = it.c_lo + warp;
+  if (pc >= f.nr) return;
+  const i64 nr = f.nr, nu = f.nu;
+  double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;  // indexed by parent row
+  const int ch0 = S.childptr[s], ch1 = S.childptr[s + 1];
+  for (int base = ch0; base < ch1; base += 32) {
+    int hit = -1;
+    const int ci = base + lane;
+    if (ci < ch1) {
+      const int c = S.child[ci];
+      const int nsc = S.col0[c + 1] - S.col0[c];
+      const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - nsc;
+      const int* rel = S.rel + S.relptr[c];
+      int lo = 0, hi = nuc;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (rel[mid] < pc)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      if (lo < nuc && rel[lo] == pc) hit = lo;
+    }
+    unsigned ballot = __ballot_sync(0xffffffffu, hit >= 0);
+    while (ballot) {
+      const int src = __ffs(ballot) - 1;
+      ballot &= ballot - 1;
+      const int cc = __shfl_sync(0xffffffffu, hit, src);
+      const int c = S.child[base + src];
+      const int nsc = S.col0[c + 1] - S.col0[c];
+      const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - nsc;
+      const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+      const int* rel = S.rel + S.relptr[c];
+      for (int r = cc + lane; r < nuc; r += 32) dstcol[rel[r]] += Ucol[r];
+    }
+  }
+}
+
+// Leaf fronts with one pivot column and at most 33 rows (the private x columns
+// of a cone block: millions of them): one warp per front.
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_leaf_factor(DevSym S, const int* list, int count, double* L, double* U, double* Dg, const double* reg,
+                  double dyn_eps, double* scalars) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int s = list[w];
+  const int c0 = S.col0[s];
+  const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]), nu = nr - 1;
+  double* Lp = L + S.Loff[s];
+  double* Up = U + S.Uoff[s];
+  double d = Lp[0];
+  if (!qs_finite(d)) {
+    if (lane == 0) scalars[SC_PIVOT_NONFINITE] = 1.0;
+  } else if (fabs(d) < dyn_eps) {
+    d = (reg[c0] >= 0.0) ? dyn_eps : -dyn_eps;
+    if (lane == 0) atomicAdd(&scalars[SC_PIVOT_BUMPS], 1.0);
+  }
+  if (lane == 0) Dg[c0] = d;
+  // lane r holds a_r = L[1+r]
+  const double a = (lane < nu) ? Lp[1 + lane] : 0.0;
+  const double l = a / d;
+  if (lane < nu) Lp[1 + lane] = l;
+  for (int j = 0; j < nu; ++j) {
+    const double lj = __shfl_sync(0xffffffffu, l, j);
+    if (lane >= j && lane < nu) Up[lane + (i64)j * nu] -= a * lj;
+  }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_leaf_fwd(DevSym S, const int* list, int count, const double* L, const double* xw, double* B) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int s = list[w];
+  const int nu = (int)(S.rowptr[s + 1] - S.rowptr[s]) - 1;
+  const double x1 = xw[S.col0[s]];
+  if (lane < nu) B[S.Boff[s] + lane] = -(L[S.Loff[s] + 1 + lane] * x1);
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_leaf_bwd(DevSym S, const int* list, int count, const double* L, double* xw) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int s = list[w];
+  const i64 rp = S.rowptr[s];
+  const int nu = (int)(S.rowptr[s + 1] - rp) - 1;
+  double acc = (lane < nu) ? L[S.Loff[s] + 1 + lane] * xw[S.rowidx[rp + 1 + lane]] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) xw[S.col0[s]] -= acc;
+}
+
+// One CTA per front of the level (children already assembled by k_extend_add):
+// factor the pivot panel, form this front's own update matrix.
 __global__ void __launch_bounds__(LDL_THREADS)
     k_front_factor(DevSym S, const int* list, double* L, double* U, double* Dg, const double* reg, double dyn_eps,
                    double* scalars) {
@@ -82,26 +186,6 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const Front f = front_of(S, s, L, U);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   const i64 nr = f.nr, nu = f.nu;
-  // ---- extend-add
-  for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci) {
-    const int c = S.child[ci];
-    const int nsc = S.col0[c + 1] - S.col0[c];
-    const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - nsc;
-    const double* Uc = U + S.Uoff[c];
-    const int* rel = S.rel + S.relptr[c];
-    for (int cc = warp; cc < nuc; cc += nwarps) {
-      const int pc = rel[cc];
-      for (int r = cc + lane; r < nuc; r += 32) {
-        const int pr = rel[r];
-        const double v = Uc[r + (i64)cc * nuc];
-        if (pc < f.ns)
-          f.Lp[pr + pc * nr] += v;
-        else
-          f.Up[(pr - f.ns) + (pc - f.ns) * nu] += v;
-      }
-    }
-    __syncthreads();
-  }
   // ---- right-looking LDL' on the pivot panel (nr x ns)
   for (int k = 0; k < f.ns; ++k) {
     __syncthreads();
@@ -258,6 +342,34 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, const i64* d_K
   UP(perm, S.perm)
 #undef UP
   d_levelsup = upload(S.levelsup, &owned, &device_bytes, st);
+  // work lists: simple leaves (warp per front), general fronts per level (CTA per front),
+  // extend-add slabs per level (8 front columns per CTA; only fronts that have children)
+  std::vector<int> leaf, gen;
+  std::vector<SlabItem> slabs;
+  genptr.assign(S.nlevels + 1, 0);
+  slabptr.assign(S.nlevels + 1, 0);
+  for (int lv = 0; lv < S.nlevels; ++lv) {
+    for (int k = S.levelptr[lv]; k < S.levelptr[lv + 1]; ++k) {
+      const int s = S.levelsup[k];
+      const int ns = S.col0[s + 1] - S.col0[s];
+      const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
+      const bool has_children = S.childptr[s + 1] > S.childptr[s];
+      if (!has_children && ns == 1 && nr <= 33) {
+        leaf.push_back(s);
+        continue;
+      }
+      gen.push_back(s);
+      if (has_children)
+        for (int c = 0; c < nr; c += 8) slabs.push_back(SlabItem{s, c});
+    }
+    genptr[lv + 1] = (int)gen.size();
+    slabptr[lv + 1] = (int)slabs.size();
+  }
+  n_leaf = (int)leaf.size();
+  d_leaf = upload(leaf, &owned, &device_bytes, st);
+  d_gen = upload(gen, &owned, &device_bytes, st);
+  d_slabs = upload(slabs, &owned, &device_bytes, st);
+  if (!d_leaf || !d_gen || !d_slabs) return "cudaMalloc failed for LDL work lists";
   std::vector<double> regh(N);
   for (i64 k = 0; k < N; ++k) regh[k] = (S.perm[k] < n_pos) ? static_reg : -static_reg;  // kkt.py:48-52
   reg = upload(regh, &owned, &device_bytes, st);
@@ -288,24 +400,45 @@ void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
   if (S.Uoff[S.nsup] > 0) cudaMemsetAsync(U, 0, S.Uoff[S.nsup] * 8, st);
   k_scatter_values<<<grid_for(knnz), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
   k_add_reg<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D, reg, L);
+  if (n_leaf > 0)
+    k_leaf_factor<<<(unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+        D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars);
   for (int lv = 0; lv < S.nlevels; ++lv) {
-    const int cnt = S.levelptr[lv + 1] - S.levelptr[lv];
-    k_front_factor<<<cnt, LDL_THREADS, 0, st>>>(D, d_levelsup + S.levelptr[lv], L, U, Dg, reg, dyn_eps, scalars);
+    const int nslab = slabptr[lv + 1] - slabptr[lv];
+    if (nslab > 0) k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
+    const int cnt = genptr[lv + 1] - genptr[lv];
+    if (cnt > 0)
+      k_front_factor<<<cnt, LDL_THREADS, 0, st>>>(D, d_gen + genptr[lv], L, U, Dg, reg, dyn_eps, scalars);
   }
 }
 
 void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
   k_permute_in<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, d_rhs, xw);
+  const unsigned leaf_grid = (unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS);
+  if (n_leaf > 0) k_leaf_fwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw, B);
   for (int lv = 0; lv < S.nlevels; ++lv) {
-    const int cnt = S.levelptr[lv + 1] - S.levelptr[lv];
-    k_solve_fwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_levelsup + S.levelptr[lv], L, xw, B);
+    const int cnt = genptr[lv + 1] - genptr[lv];
+    if (cnt > 0) k_solve_fwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_gen + genptr[lv], L, xw, B);
   }
   k_solve_diag<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, Dg, xw);
   for (int lv = S.nlevels - 1; lv >= 0; --lv) {
-    const int cnt = S.levelptr[lv + 1] - S.levelptr[lv];
-    k_solve_bwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_levelsup + S.levelptr[lv], L, xw);
+    const int cnt = genptr[lv + 1] - genptr[lv];
+    if (cnt > 0) k_solve_bwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_gen + genptr[lv], L, xw);
   }
+  if (n_leaf > 0) k_leaf_bwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw);
   k_permute_out<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, xw, d_sol);
+}
+
+int LinSys::launches_per_factor() const {
+  int k = 4 + (n_leaf > 0);
+  for (int lv = 0; lv < S.nlevels; ++lv) k += (slabptr[lv + 1] > slabptr[lv]) + (genptr[lv + 1] > genptr[lv]);
+  return k;
+}
+
+int LinSys::launches_per_solve() const {
+  int k = 3 + 2 * (n_leaf > 0);
+  for (int lv = 0; lv < S.nlevels; ++lv) k += 2 * (genptr[lv + 1] > genptr[lv]);
+  return k;
 }
 
 void LinSys::release() {

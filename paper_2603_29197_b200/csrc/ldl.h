@@ -36,6 +36,11 @@ struct DevSym {
   const int* perm;
 };
 
+// extend-add work item: front `front`, columns [c_lo, c_lo + 8)
+struct SlabItem {
+  int front, c_lo;
+};
+
 struct LinSys {
   Symbolic S;
   DevSym D{};
@@ -49,6 +54,12 @@ struct LinSys {
   double* reg = nullptr;   // sign-matched static shift per new column
   i64* amap = nullptr;     // K entry -> panel storage offset
   int* d_levelsup = nullptr;
+  // work lists built at analysis (see ldl.cu)
+  int n_leaf = 0;
+  int* d_leaf = nullptr;
+  int* d_gen = nullptr;
+  SlabItem* d_slabs = nullptr;
+  std::vector<int> genptr, slabptr;
   std::vector<void*> owned;
   double dyn_eps = 1e-14;
   double analysis_seconds = 0.0;
@@ -60,5 +71,7 @@ struct LinSys {
                       double static_reg, cudaStream_t st);
   void factor(const double* d_Kx, double* scalars, cudaStream_t st);
   void solve(const double* d_rhs, double* d_sol, cudaStream_t st);  // (L D L')^{-1} rhs, no refinement
+  int launches_per_factor() const;
+  int launches_per_solve() const;
   void release();
 };

@@ -93,7 +93,8 @@ def _symbolic(kkt, ordering, cone=None, user_perm=None):
 
 
 @pytest.mark.parametrize("name", golden_problem_names())
-def test_symbolic_analysis_is_valid_and_counts_match_oracle(oracle, name):
+def test_symbolic_analysis_is_valid_and_counts_match_oracle(oracle, name, monkeypatch):
+    monkeypatch.setenv("QS_RELAX", "0")  # exact supernodes: no padded zeros in the count
     g = load_golden(name)
     d = problem_from_golden(g)
     kkt = assemble_kkt(d)
@@ -106,6 +107,17 @@ def test_symbolic_analysis_is_valid_and_counts_match_oracle(oracle, name):
             sym = oracle.symbolic_factor(oracle._csc(kkt.matrix), perm)
             assert int(st["lnz"]) == sym.Li.size + N, (ordering, cone is not None)
             assert 1 <= st["nsup"] <= N and st["max_nr"] <= N
+
+
+def test_relaxed_amalgamation_pads_but_never_loses_entries(monkeypatch):
+    d = problem_from_golden(load_golden("group_lasso_3"))
+    kkt = assemble_kkt(d)
+    monkeypatch.setenv("QS_RELAX", "0")
+    _, exact = _symbolic(kkt, 1, d.cone)
+    monkeypatch.setenv("QS_RELAX", "0.4")
+    _, relaxed = _symbolic(kkt, 1, d.cone)
+    assert relaxed["nsup"] <= exact["nsup"] and relaxed["lnz"] >= exact["lnz"]
+    assert relaxed["lnz"] <= 2.0 * exact["lnz"]
 
 
 def test_amd_reduces_fill_on_an_arrow_matrix():
