@@ -365,12 +365,18 @@ def write_scaling(kkt: KKT, sc: Scaling) -> None:  # kkt.py:146-150
 
 
 # -------------------------------------------------------------------- ldl ----
-def default_perm(K) -> np.ndarray:
+def default_perm(K, kkt=None, cone=None) -> np.ndarray:
     """Fill-reducing order.  See the module docstring for why this is not the
-    reference's `_amd.py`."""
+    reference's `_amd.py`.  When the cone layout is known the SOC blocks are
+    handed over as cliques, so the CPU baseline factorises with the same
+    (best available) ordering as the GPU path."""
     try:
         from paper_2603_29197_b200 import ordering as _ord
 
+        if kkt is not None and cone is not None and len(cone.soc_dims):
+            starts, dims = soc_layout(cone)
+            return _ord.analyze(K.cols, K.col_pointers, K.row_indices, "amd", None,
+                                starts + kkt.n + kkt.p, dims)[0]
         return _ord.amd_order_upper(K.cols, K.col_pointers, K.row_indices)
     except Exception:
         return np.arange(K.cols, dtype=_i64)
@@ -467,11 +473,11 @@ def solve_refine(fac, sym, K, rhs, refine_iters) -> np.ndarray:  # ldl.py:135-16
 
 
 class Backend:  # linsys.py:54-108 (BuiltinBackend)
-    def __init__(self, kkt: KKT, settings, perm=None):
+    def __init__(self, kkt: KKT, settings, perm=None, cone=None):
         self.kkt, self.settings = kkt, settings
         self.n_factor = self.n_solve = 0
         t = time.perf_counter()
-        fwd = default_perm(kkt.matrix) if perm is None else np.asarray(perm, dtype=_i64)
+        fwd = default_perm(kkt.matrix, kkt, cone) if perm is None else np.asarray(perm, dtype=_i64)
         self.sym = symbolic_factor(kkt.matrix, fwd)
         self.analysis_seconds = time.perf_counter() - t
         self.signs = reg_signs(kkt.n, kkt.p, kkt.m)
@@ -636,7 +642,7 @@ def solve(data, settings=None, perm=None, hook=None, trace=None) -> OracleResult
     d = SimpleNamespace(n=data.n, m=data.m, p=data.p, P=_csc(data.P), A=_csc(data.A), G=_csc(data.G),
                         c=_vec(data.c), b=_vec(data.b), h=_vec(data.h), cone=data.cone)
     kkt = assemble_kkt(d)
-    backend = Backend(kkt, st, perm)
+    backend = Backend(kkt, st, perm, d.cone)
     t1 = time.perf_counter()
     status, iters, stalls = "NumericalError", 0, 0
     it = Iterate(np.zeros(d.n), np.zeros(d.p), np.zeros(d.m), np.zeros(d.m), 0.0)

@@ -21,6 +21,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", 
               "-Xcompiler", "-fPIC"]
 CU = ["cone_kernels.cu", "kkt_kernels.cu", "spmv_kernels.cu", "ldl.cu", "capi.cu"]
 CPP = ["host_setup.cpp"]
+FMA_OK = {"ldl.cu"}  # the factorisation is not a restatement of reference arithmetic: let it use FMA
 
 
 def _stale(target, deps):
@@ -43,7 +44,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     for f in CU:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         if force or _stale(obj, [src] + hdrs):
-            jobs.append([NVCC, *NVCC_FLAGS, "-c", src, "-o", obj])
+            flags = [x for x in NVCC_FLAGS if not (f in FMA_OK and x == "-fmad=false")]
+            jobs.append([NVCC, *flags, "-c", src, "-o", obj])
     for f in CPP:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         if force or _stale(obj, [src] + hdrs):

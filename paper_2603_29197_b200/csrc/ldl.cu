@@ -222,6 +222,328 @@ __global__ void __launch_bounds__(LDL_THREADS)
   }
 }
 
+// ============================ blocked path for large fronts ==================
+// Fronts too large for one CTA are factored by panels of NB = 32 pivot columns,
+// every front of the level advancing in lockstep (blockIdx.y = front):
+//   k_blk_diag    factor the NB x NB diagonal block (one CTA per front)
+//   k_blk_panel   rows below it: L21 = A21 L11^-T D^-1 (thread per row)
+//   k_blk_update  rank-NB update of the remaining pivot columns (64x64 tiles)
+// and, once the panel is done, k_blk_update in SCHUR mode forms the front's
+// update matrix U -= L21 D L21' with the full pivot depth.
+#define NB 32
+#define TS 64  // update tile edge
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_blk_diag(DevSym S, const int* list, int kb, double* L, double* Dg, const double* reg, double dyn_eps,
+               double* scalars) {
+  const int s = list[blockIdx.x];
+  const Front f = front_of(S, s, L, nullptr);
+  if (kb >= f.ns) return;
+  const int nb = min(NB, f.ns - kb);
+  const i64 nr = f.nr;
+  __shared__ double a[NB][NB + 1];
+  __shared__ double dsh[NB];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    a[i][j] = (i >= j) ? f.Lp[(kb + i) + (i64)(kb + j) * nr] : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
+    double d = a[k][k];
+    __syncthreads();
+    if (!qs_finite(d)) {
+      if (tid == 0) scalars[SC_PIVOT_NONFINITE] = 1.0;
+    } else if (fabs(d) < dyn_eps) {
+      d = (reg[f.c0 + kb + k] >= 0.0) ? dyn_eps : -dyn_eps;
+      if (tid == 0) atomicAdd(&scalars[SC_PIVOT_BUMPS], 1.0);
+    }
+    if (tid == 0) dsh[k] = d;
+    // trailing update inside the block: a[i][j] -= a[i][k] * a[j][k] / d, k < j <= i
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int i = e % nb, j = e / nb;
+      if (j > k && i >= j) a[i][j] -= a[i][k] * (a[j][k] / d);
+    }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < nb; i += blockDim.x) a[i][k] /= d;
+    __syncthreads();
+  }
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    if (i > j) f.Lp[(kb + i) + (i64)(kb + j) * nr] = a[i][j];
+  }
+  for (int k = tid; k < nb; k += blockDim.x) {
+    Dg[f.c0 + kb + k] = dsh[k];
+    f.Lp[(kb + k) + (i64)(kb + k) * nr] = dsh[k];
+  }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_blk_panel(DevSym S, const int* list, int kb, double* L, const double* Dg) {
+  const int s = list[blockIdx.y];
+  const Front f = front_of(S, s, L, nullptr);
+  if (kb >= f.ns) return;
+  const int nb = min(NB, f.ns - kb);
+  const int row0 = kb + nb + blockIdx.x * blockDim.x;
+  if (row0 >= f.nr) return;
+  const i64 nr = f.nr;
+  __shared__ double l11[NB][NB + 1];
+  __shared__ double dinv[NB];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    l11[i][j] = (i > j) ? f.Lp[(kb + i) + (i64)(kb + j) * nr] : 0.0;
+  }
+  for (int k = tid; k < nb; k += blockDim.x) dinv[k] = 1.0 / Dg[f.c0 + kb + k];
+  __syncthreads();
+  const int row = row0 + tid;
+  if (row >= f.nr) return;
+  double y[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) y[k] = (k < nb) ? f.Lp[row + (i64)(kb + k) * nr] : 0.0;
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    if (k < nb) {
+      double acc = y[k];
+#pragma unroll
+      for (int mm = 0; mm < NB; ++mm)
+        if (mm < k) acc -= y[mm] * l11[k][mm];
+      y[k] = acc;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k)
+    if (k < nb) f.Lp[row + (i64)(kb + k) * nr] = y[k] * dinv[k];
+}
+
+// C(i, j) -= sum_k A(i, k) d_k A(j, k) over 64 x 64 tiles of the lower triangle.
+//   PANEL mode: C = panel columns [kb+nb, ns), rows [col, nr); k in [kb, kb+nb)
+//   SCHUR mode: C = U (nu x nu);                              k in [0, ns)
+template <bool SCHUR>
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_blk_update(DevSym S, const int* list, int kb, double* L, double* U, const double* Dg) {
+  const int s = list[blockIdx.y];
+  const Front f = front_of(S, s, L, U);
+  int k_lo, k_hi, c_lo, c_hi;
+  if (SCHUR) {
+    k_lo = 0;
+    k_hi = f.ns;
+    c_lo = f.ns;
+    c_hi = f.nr;
+  } else {
+    if (kb >= f.ns) return;
+    k_lo = kb;
+    k_hi = min(f.ns, kb + NB);
+    c_lo = k_hi;
+    c_hi = f.ns;
+  }
+  if (c_lo >= c_hi || k_lo >= k_hi) return;
+  const int ntj = (c_hi - c_lo + TS - 1) / TS;
+  const int nti = (f.nr - c_lo + TS - 1) / TS;
+  if ((int)blockIdx.x >= nti * ntj) return;
+  const int tj = blockIdx.x / nti, ti = blockIdx.x % nti;
+  const int i0 = c_lo + ti * TS, j0 = c_lo + tj * TS;  // front-local row / column of the tile origin
+  if (i0 + TS <= j0) return;                         // entirely above the diagonal
+  const i64 nr = f.nr;
+  __shared__ double As[NB][TS + 2];
+  __shared__ double Bs[NB][TS + 2];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = k_lo; k0 < k_hi; k0 += NB) {
+    const int kn = min(NB, k_hi - k0);
+    // stage A(i0.., k0..) and d_k * A(j0.., k0..): consecutive threads read consecutive rows (coalesced)
+    for (int e = tid; e < NB * TS; e += blockDim.x) {
+      const int r = e % TS, k = e / TS;
+      const int gi = i0 + r, gj = j0 + r;
+      double va = 0.0, vb = 0.0;
+      if (k < kn) {
+        if (gi < f.nr) va = f.Lp[gi + (i64)(k0 + k) * nr];
+        if (gj < c_hi) vb = f.Lp[gj + (i64)(k0 + k) * nr] * Dg[f.c0 + k0 + k];
+      }
+      As[k][r] = va;
+      Bs[k][r] = vb;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < NB; ++k) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[k][tx + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[k][ty + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int gj = j0 + ty + 16 * b;
+    if (gj >= c_hi) continue;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int gi = i0 + tx + 16 * a;
+      if (gi >= f.nr || gi < gj) continue;
+      if (SCHUR)
+        f.Up[(gi - f.ns) + (i64)(gj - f.ns) * f.nu] -= acc[a][b];
+      else
+        f.Lp[gi + (i64)gj * nr] -= acc[a][b];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS) k_zero_cb(DevSym S, const int* list, double* B) {
+  const int s = list[blockIdx.x];
+  if (S.childptr[s + 1] != S.childptr[s]) return;
+  const int nu = (int)(S.rowptr[s + 1] - S.rowptr[s]) - (S.col0[s + 1] - S.col0[s]);
+  for (int r = threadIdx.x; r < nu; r += blockDim.x) B[S.Boff[s] + r] = 0.0;
+}
+
+// ---- forward-solve gather: contributions of the children into a front, same
+// ownership scheme as k_extend_add (warp w of a slab owns front row c_lo + w).
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_gather_fwd(DevSym S, const SlabItem* items, double* xw, double* B) {
+  const SlabItem it = items[blockIdx.x];
+  const int s = it.front;
+  const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
+  const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pr = it.c_lo + warp;
+  if (pr >= nr) return;
+  double acc = 0.0;
+  const int ch0 = S.childptr[s], ch1 = S.childptr[s + 1];
+  for (int base = ch0; base < ch1; base += 32) {
+    double v = 0.0;
+    const int ci = base + lane;
+    if (ci < ch1) {
+      const int c = S.child[ci];
+      const int nsc = S.col0[c + 1] - S.col0[c];
+      const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - nsc;
+      const int* rel = S.rel + S.relptr[c];
+      int lo = 0, hi = nuc;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (rel[mid] < pr)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      if (lo < nuc && rel[lo] == pr) v = B[S.Boff[c] + lo];
+    }
+    // fixed-order sum over the 32 children of this batch
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc += v;
+  }
+  if (lane == 0) {
+    if (pr < ns)
+      xw[c0 + pr] += acc;
+    else
+      B[S.Boff[s] + pr - ns] = acc;
+  }
+}
+
+// ---- blocked triangular solves for the large fronts (lockstep over the level)
+__global__ void __launch_bounds__(32) k_fwd_diag(DevSym S, const int* list, int kb, const double* L, double* xw) {
+  const int s = list[blockIdx.x];
+  const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
+  if (kb >= ns) return;
+  const int nb = min(NB, ns - kb);
+  const i64 nr = S.rowptr[s + 1] - S.rowptr[s];
+  const double* Lp = L + S.Loff[s];
+  const int lane = threadIdx.x;
+  double x = (lane < nb) ? xw[c0 + kb + lane] : 0.0;
+  for (int k = 0; k < nb - 1; ++k) {
+    const double xk = __shfl_sync(0xffffffffu, x, k);
+    if (lane > k && lane < nb) x -= Lp[(kb + lane) + (i64)(kb + k) * nr] * xk;
+  }
+  if (lane < nb) xw[c0 + kb + lane] = x;
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_fwd_update(DevSym S, const int* list, int kb, const double* L, double* xw, double* B) {
+  const int s = list[blockIdx.y];
+  const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
+  if (kb >= ns) return;
+  const int nb = min(NB, ns - kb);
+  const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
+  const int row0 = kb + nb + blockIdx.x * blockDim.x;
+  if (row0 >= nr) return;
+  __shared__ double xs[NB];
+  if (threadIdx.x < NB) xs[threadIdx.x] = (threadIdx.x < nb) ? xw[c0 + kb + threadIdx.x] : 0.0;
+  __syncthreads();
+  const int r = row0 + threadIdx.x;
+  if (r >= nr) return;
+  const double* Lp = L + S.Loff[s] + r + (i64)kb * nr;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < nb; ++k) acc += Lp[(i64)k * nr] * xs[k];
+  if (r < ns)
+    xw[c0 + r] -= acc;
+  else
+    B[S.Boff[s] + r - ns] -= acc;
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_bwd_partial(DevSym S, const int* list, const i64* poff, int kb, const double* L, const double* xw,
+                  double* partial) {
+  const int s = list[blockIdx.y];
+  const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
+  if (kb >= ns) return;
+  const int nb = min(NB, ns - kb);
+  const i64 rp = S.rowptr[s];
+  const int nr = (int)(S.rowptr[s + 1] - rp);
+  const int row0 = kb + nb + blockIdx.x * blockDim.x;
+  if (row0 >= nr) return;
+  const int r = row0 + threadIdx.x;
+  __shared__ double red[LDL_THREADS / 32][NB];
+  double xr = 0.0;
+  const double* Lp = L + S.Loff[s] + (i64)kb * nr;
+  if (r < nr) xr = (r < ns) ? xw[c0 + r] : xw[S.rowidx[rp + r]];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = 0; k < nb; ++k) {
+    double v = (r < nr) ? Lp[r + (i64)k * nr] * xr : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    double t = 0.0;
+    for (int w = 0; w < LDL_THREADS / 32; ++w) t += red[w][threadIdx.x];
+    partial[poff[blockIdx.y] + (i64)blockIdx.x * NB + threadIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(32)
+    k_bwd_diag(DevSym S, const int* list, const i64* poff, int kb, const double* L, double* xw,
+               const double* partial) {
+  const int s = list[blockIdx.x];
+  const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
+  if (kb >= ns) return;
+  const int nb = min(NB, ns - kb);
+  const i64 nr = S.rowptr[s + 1] - S.rowptr[s];
+  const double* Lp = L + S.Loff[s];
+  const int lane = threadIdx.x;
+  const int rows_below = (int)nr - kb - nb;
+  const int ntiles = rows_below > 0 ? (rows_below + LDL_THREADS - 1) / LDL_THREADS : 0;
+  double x = (lane < nb) ? xw[c0 + kb + lane] : 0.0;
+  if (lane < nb)
+    for (int t = 0; t < ntiles; ++t) x -= partial[poff[blockIdx.x] + (i64)t * NB + lane];
+  for (int k = nb - 1; k > 0; --k) {
+    const double xk = __shfl_sync(0xffffffffu, x, k);
+    if (lane < k) x -= Lp[(kb + k) + (i64)(kb + lane) * nr] * xk;
+  }
+  if (lane < nb) xw[c0 + kb + lane] = x;
+}
+
 // ---- triangular solves, one CTA per front of the level
 __global__ void __launch_bounds__(LDL_THREADS)
     k_solve_fwd(DevSym S, const int* list, const double* L, double* xw, double* B) {
@@ -230,21 +552,8 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const int tid = threadIdx.x;
   const i64 nr = f.nr;
   double* cb = B + S.Boff[s];
-  for (int r = tid; r < f.nu; r += blockDim.x) cb[r] = 0.0;
-  __syncthreads();
-  for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci) {
-    const int c = S.child[ci];
-    const int nsc = S.col0[c + 1] - S.col0[c];
-    const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - nsc;
-    const double* cbc = B + S.Boff[c];
-    const int* rel = S.rel + S.relptr[c];
-    for (int r = tid; r < nuc; r += blockDim.x) {
-      const int pr = rel[r];
-      if (pr < f.ns)
-        xw[f.c0 + pr] += cbc[r];
-      else
-        cb[pr - f.ns] += cbc[r];
-    }
+  if (S.childptr[s + 1] == S.childptr[s]) {  // no children: nothing was gathered, start from zero
+    for (int r = tid; r < f.nu; r += blockDim.x) cb[r] = 0.0;
     __syncthreads();
   }
   double* x1 = xw + f.c0;
@@ -344,8 +653,13 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, const i64* d_K
   d_levelsup = upload(S.levelsup, &owned, &device_bytes, st);
   // work lists: simple leaves (warp per front), general fronts per level (CTA per front),
   // extend-add slabs per level (8 front columns per CTA; only fronts that have children)
-  std::vector<int> leaf, gen;
+  std::vector<int> leaf, gen, small, blk;
   std::vector<SlabItem> slabs;
+  smallptr.assign(S.nlevels + 1, 0);
+  blkptr.assign(S.nlevels + 1, 0);
+  blk_max_ns.assign(S.nlevels, 0);
+  blk_max_nr.assign(S.nlevels, 0);
+  blk_max_nu.assign(S.nlevels, 0);
   genptr.assign(S.nlevels + 1, 0);
   slabptr.assign(S.nlevels + 1, 0);
   for (int lv = 0; lv < S.nlevels; ++lv) {
@@ -359,17 +673,46 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, const i64* d_K
         continue;
       }
       gen.push_back(s);
+      if (nr > 96 || ns > 48) {
+        blk.push_back(s);
+        blk_max_ns[lv] = std::max(blk_max_ns[lv], ns);
+        blk_max_nr[lv] = std::max(blk_max_nr[lv], nr);
+        blk_max_nu[lv] = std::max(blk_max_nu[lv], nr - ns);
+      } else {
+        small.push_back(s);
+      }
       if (has_children)
         for (int c = 0; c < nr; c += 8) slabs.push_back(SlabItem{s, c});
     }
     genptr[lv + 1] = (int)gen.size();
+    smallptr[lv + 1] = (int)small.size();
+    blkptr[lv + 1] = (int)blk.size();
     slabptr[lv + 1] = (int)slabs.size();
   }
   n_leaf = (int)leaf.size();
   d_leaf = upload(leaf, &owned, &device_bytes, st);
   d_gen = upload(gen, &owned, &device_bytes, st);
+  d_small = upload(small, &owned, &device_bytes, st);
+  d_blk = upload(blk, &owned, &device_bytes, st);
+  // per blocked front: offset of its row-tile partial sums (backward solve); the workspace is reused per level
+  std::vector<i64> poff(blk.size() + 1, 0);
+  i64 pmax = 0;
+  for (int lv = 0; lv < S.nlevels; ++lv) {
+    i64 at = 0;
+    for (int k = blkptr[lv]; k < blkptr[lv + 1]; ++k) {
+      const int fs = blk[k];
+      const i64 nrf = S.rowptr[fs + 1] - S.rowptr[fs];
+      poff[k] = at;
+      at += ((nrf + LDL_THREADS - 1) / LDL_THREADS) * NB;
+    }
+    pmax = std::max(pmax, at);
+  }
+  d_poff = upload(poff, &owned, &device_bytes, st);
+  if (cudaMalloc((void**)&partial, std::max<i64>(pmax, 1) * 8) != cudaSuccess) return "cudaMalloc failed (solve partials)";
+  owned.push_back(partial);
+  device_bytes += pmax * 8;
   d_slabs = upload(slabs, &owned, &device_bytes, st);
-  if (!d_leaf || !d_gen || !d_slabs) return "cudaMalloc failed for LDL work lists";
+  if (!d_leaf || !d_gen || !d_small || !d_blk || !d_slabs) return "cudaMalloc failed for LDL work lists";
   std::vector<double> regh(N);
   for (i64 k = 0; k < N; ++k) regh[k] = (S.perm[k] < n_pos) ? static_reg : -static_reg;  // kkt.py:48-52
   reg = upload(regh, &owned, &device_bytes, st);
@@ -406,9 +749,35 @@ void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
   for (int lv = 0; lv < S.nlevels; ++lv) {
     const int nslab = slabptr[lv + 1] - slabptr[lv];
     if (nslab > 0) k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
-    const int cnt = genptr[lv + 1] - genptr[lv];
+    const int cnt = smallptr[lv + 1] - smallptr[lv];
     if (cnt > 0)
-      k_front_factor<<<cnt, LDL_THREADS, 0, st>>>(D, d_gen + genptr[lv], L, U, Dg, reg, dyn_eps, scalars);
+      k_front_factor<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, U, Dg, reg, dyn_eps, scalars);
+    // blocked fronts of this level, in chunks that fit gridDim.y
+    for (int b0 = blkptr[lv]; b0 < blkptr[lv + 1]; b0 += 65535) {
+      const int nb_fronts = std::min(65535, blkptr[lv + 1] - b0);
+      const int* lst = d_blk + b0;
+      const int mx_ns = blk_max_ns[lv], mx_nr = blk_max_nr[lv];
+      for (int kb = 0; kb < mx_ns; kb += NB) {
+        k_blk_diag<<<nb_fronts, LDL_THREADS, 0, st>>>(D, lst, kb, L, Dg, reg, dyn_eps, scalars);
+        const int rows_below = mx_nr - kb - 1;
+        if (rows_below > 0) {
+          dim3 gp((rows_below + LDL_THREADS - 1) / LDL_THREADS, nb_fronts);
+          k_blk_panel<<<gp, LDL_THREADS, 0, st>>>(D, lst, kb, L, Dg);
+        }
+        const int cols_left = mx_ns - kb - 1;
+        if (cols_left > 0) {
+          const int ntj = (cols_left + TS - 1) / TS, nti = (mx_nr - kb - 1 + TS - 1) / TS;
+          dim3 gu(ntj * nti, nb_fronts);
+          k_blk_update<false><<<gu, LDL_THREADS, 0, st>>>(D, lst, kb, L, U, Dg);
+        }
+      }
+      const int mx_nu = blk_max_nu[lv];
+      if (mx_nu > 0) {
+        const int nt = (mx_nu + TS - 1) / TS;
+        dim3 gu(nt * nt, nb_fronts);
+        k_blk_update<true><<<gu, LDL_THREADS, 0, st>>>(D, lst, 0, L, U, Dg);
+      }
+    }
   }
 }
 
@@ -417,27 +786,69 @@ void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
   const unsigned leaf_grid = (unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS);
   if (n_leaf > 0) k_leaf_fwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw, B);
   for (int lv = 0; lv < S.nlevels; ++lv) {
-    const int cnt = genptr[lv + 1] - genptr[lv];
-    if (cnt > 0) k_solve_fwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_gen + genptr[lv], L, xw, B);
+    const int nslab = slabptr[lv + 1] - slabptr[lv];
+    if (nslab > 0) k_gather_fwd<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], xw, B);
+    const int cnt = smallptr[lv + 1] - smallptr[lv];
+    if (cnt > 0) k_solve_fwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw, B);
+    for (int b0 = blkptr[lv]; b0 < blkptr[lv + 1]; b0 += 65535) {
+      const int nbf = std::min(65535, blkptr[lv + 1] - b0);
+      const int* lst = d_blk + b0;
+      // childless blocked fronts start their contribution vector from zero (the others were set by the gather)
+      k_zero_cb<<<nbf, LDL_THREADS, 0, st>>>(D, lst, B);
+      for (int kb = 0; kb < blk_max_ns[lv]; kb += NB) {
+        k_fwd_diag<<<nbf, 32, 0, st>>>(D, lst, kb, L, xw);
+        const int rows_below = blk_max_nr[lv] - kb - 1;
+        if (rows_below > 0) {
+          dim3 g((rows_below + LDL_THREADS - 1) / LDL_THREADS, nbf);
+          k_fwd_update<<<g, LDL_THREADS, 0, st>>>(D, lst, kb, L, xw, B);
+        }
+      }
+    }
   }
   k_solve_diag<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, Dg, xw);
   for (int lv = S.nlevels - 1; lv >= 0; --lv) {
-    const int cnt = genptr[lv + 1] - genptr[lv];
-    if (cnt > 0) k_solve_bwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_gen + genptr[lv], L, xw);
+    for (int b0 = blkptr[lv]; b0 < blkptr[lv + 1]; b0 += 65535) {
+      const int nbf = std::min(65535, blkptr[lv + 1] - b0);
+      const int* lst = d_blk + b0;
+      const i64* po = d_poff + b0;
+      const int last_kb = ((blk_max_ns[lv] - 1) / NB) * NB;
+      for (int kb = last_kb; kb >= 0; kb -= NB) {
+        const int rows_below = blk_max_nr[lv] - kb - 1;
+        if (rows_below > 0) {
+          dim3 g((rows_below + LDL_THREADS - 1) / LDL_THREADS, nbf);
+          k_bwd_partial<<<g, LDL_THREADS, 0, st>>>(D, lst, po, kb, L, xw, partial);
+        }
+        k_bwd_diag<<<nbf, 32, 0, st>>>(D, lst, po, kb, L, xw, partial);
+      }
+    }
+    const int cnt = smallptr[lv + 1] - smallptr[lv];
+    if (cnt > 0) k_solve_bwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw);
   }
   if (n_leaf > 0) k_leaf_bwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw);
   k_permute_out<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, xw, d_sol);
 }
 
 int LinSys::launches_per_factor() const {
-  int k = 4 + (n_leaf > 0);
-  for (int lv = 0; lv < S.nlevels; ++lv) k += (slabptr[lv + 1] > slabptr[lv]) + (genptr[lv + 1] > genptr[lv]);
+  int k = 2 + (n_leaf > 0);  // own kernels only (the two memsets are not counted)
+  for (int lv = 0; lv < S.nlevels; ++lv) {
+    k += (slabptr[lv + 1] > slabptr[lv]) + (smallptr[lv + 1] > smallptr[lv]);
+    if (blkptr[lv + 1] > blkptr[lv]) {
+      const int chunks = (blkptr[lv + 1] - blkptr[lv] + 65534) / 65535;
+      k += chunks * (3 * ((blk_max_ns[lv] + NB - 1) / NB) + 1);
+    }
+  }
   return k;
 }
 
 int LinSys::launches_per_solve() const {
   int k = 3 + 2 * (n_leaf > 0);
-  for (int lv = 0; lv < S.nlevels; ++lv) k += 2 * (genptr[lv + 1] > genptr[lv]);
+  for (int lv = 0; lv < S.nlevels; ++lv) {
+    k += (slabptr[lv + 1] > slabptr[lv]) + 2 * (smallptr[lv + 1] > smallptr[lv]);
+    if (blkptr[lv + 1] > blkptr[lv]) {
+      const int chunks = (blkptr[lv + 1] - blkptr[lv] + 65534) / 65535;
+      k += chunks * (1 + 4 * ((blk_max_ns[lv] + NB - 1) / NB));
+    }
+  }
   return k;
 }
 

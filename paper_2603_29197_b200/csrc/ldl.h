@@ -59,7 +59,11 @@ struct LinSys {
   int* d_leaf = nullptr;
   int* d_gen = nullptr;
   SlabItem* d_slabs = nullptr;
-  std::vector<int> genptr, slabptr;
+  int* d_small = nullptr;  // general fronts factored by one CTA
+  int* d_blk = nullptr;    // general fronts factored by the blocked multi-CTA path
+  i64* d_poff = nullptr;   // per blocked front: offset into `partial`
+  double* partial = nullptr;  // backward-solve row-tile partial sums
+  std::vector<int> genptr, slabptr, smallptr, blkptr, blk_max_ns, blk_max_nr, blk_max_nu;
   std::vector<void*> owned;
   double dyn_eps = 1e-14;
   double analysis_seconds = 0.0;

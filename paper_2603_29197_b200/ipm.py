@@ -99,6 +99,10 @@ class DeviceSolver:
     def _check(self, rc, what=""):
         _lib.check(self.lib, self.h, rc, what)
 
+    def set_stream(self, cuda_stream: int):
+        """Run on an existing CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(self.lib.qs_set_stream(self.h, C.c_void_p(cuda_stream)))
+
     # -- IPM phases (each is one C-ABI call)
     def initialize_iterate(self) -> float:  # ipm.py:135-156
         mu = C.c_double()
