@@ -536,6 +536,8 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   h->d_slot_start = h->cone_pool.upload(slot_start.data(), slot_start.size(), h->stream);
   P.slot_start = h->d_slot_start;
   P.kp_conic = nullptr;
+  P.g_ptr = nullptr;
+  P.g_val = nullptr;
   P.c4 = h->cone_pool.alloc<double>(nsoc);
   P.e2 = h->cone_pool.alloc<double>(nsoc);
   h->cone_tmp = h->cone_pool.alloc<double>(m);
@@ -758,6 +760,8 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   if (!h->c || !h->b || !h->hv || !h->d_Kp || !h->d_Ki || !h->d_Kx || !h->d_pos)
     return fail(h, QS_E_MEMORY, "out of device memory for the KKT system");
   h->wp.kp_conic = h->d_Kp + n + p + 1;
+  h->wp.g_ptr = h->Gr.ptr;
+  h->wp.g_val = h->Gr.val;
   // closed-form map == explicit map?
   {
     int* flag = h->prob_pool.alloc<int>(1);

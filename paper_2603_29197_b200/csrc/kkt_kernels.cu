@@ -41,25 +41,26 @@ __global__ void __launch_bounds__(QS_THREADS) k_wtw_prepass(int nsoc, const int*
   }
 }
 
-// Per-column constants staged once per tile.  With A = -eta^2 (4c+4) w_j every
-// tail-tail entry is A*w_i; row 0 uses A0 = -eta^2 4c w_j, the (0,0) entry
+// Per-column constants, staged once per tile as structure-of-arrays in shared
+// memory.  With A = -eta^2 (4c+4) w_j every tail-tail entry of column j is
+// A * w_i; row 0 uses A0 = -eta^2 4c w_j, the (0,0) entry is
 // -eta^2((4c-4) w_0^2 + 1), the diagonal adds -eta^2.  Algebraically identical
 // to _cone_kernels.py:176-185 (the +-2 w_i w_j terms cancel or double); it
 // differs from the reference's expression by rounding only (<= a few ulp).
-struct ColMeta {
-  double A, A0, ne2;
-  i64 base;  // destination of row 0 of this column
-  int j;     // local column index inside its cone
-  int woff;  // offset of the cone's wbar inside the staged window
-};
-
-template <int MODE>
+//
+// Streaming phase: HALF a warp per column (two adjacent columns per warp, whose
+// lengths differ by one, so the two halves stay in step): the average column of
+// the C4 layout has 68 entries, and 16-lane groups waste fewer lanes and halve
+// the per-column instruction overhead per warp instruction.  Each 16-lane store
+// is a contiguous 128-byte run.
+template <int MODE, bool STAGED>
 __global__ void __launch_bounds__(QS_THREADS)
     k_neg_wtw(int l, int nb_orth, int max_cols, int wcap, const double* __restrict__ w,
               const double* __restrict__ wbar, const int* __restrict__ soc_ptr, const int* __restrict__ cone_of_col,
               const int* __restrict__ tile_ptr, const double* __restrict__ c4, const double* __restrict__ e2,
               const i64* __restrict__ slot_start, const i64* __restrict__ positions,
-              const i64* __restrict__ kp_conic, double* __restrict__ out) {
+              const i64* __restrict__ kp_conic, const int* __restrict__ g_ptr, const double* __restrict__ g_val,
+              double* __restrict__ out) {
   if ((int)blockIdx.x < nb_orth) {
     // orthant diagonal: slot i holds -(w_i^2)                    (cones.py:324-326)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l; i += nb_orth * blockDim.x) {
@@ -71,69 +72,66 @@ __global__ void __launch_bounds__(QS_THREADS)
     return;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ColMeta* meta = reinterpret_cast<ColMeta*>(smem_raw);
-  double* wst = reinterpret_cast<double*>(smem_raw + (size_t)max_cols * sizeof(ColMeta));
+  double* mA = reinterpret_cast<double*>(smem_raw);
+  double* mA0 = mA + max_cols;
+  double* mne2 = mA0 + max_cols;
+  i64* mbase = reinterpret_cast<i64*>(mne2 + max_cols);
+  int* mj = reinterpret_cast<int*>(mbase + max_cols);
+  int* mwoff = mj + max_cols;
+  double* wst = reinterpret_cast<double*>(mwoff + max_cols);  // 2 * max_cols ints: 8-byte aligned
   const int tile = blockIdx.x - nb_orth;
   const int col0 = tile_ptr[tile], col1 = tile_ptr[tile + 1];
   const int ncols = col1 - col0;
   // window of wbar covering every cone touched by the tile: [wlo, col1)
   const int wlo = soc_ptr[cone_of_col[col0 - l]];
   const int wlen = col1 - wlo;
-  const bool staged = wlen <= wcap;
-  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+  for (int c = threadIdx.x; c < ncols; c += QS_THREADS) {
     const int col = col0 + c;
     const int k = cone_of_col[col - l];
     const int o = soc_ptr[k];
     const int j = col - o;
     const double cc = c4[k], ne2 = -e2[k], wj = wbar[col];
-    ColMeta m;
-    m.ne2 = ne2;
-    m.j = j;
-    m.woff = o - wlo;
-    if (j == 0) {
-      m.A = 0.0;
-      m.A0 = ne2 * ((cc - 4.0) * wj);  // times w_0 below, then the diagonal term
-    } else {
-      m.A = ne2 * ((cc + 4.0) * wj);
-      m.A0 = ne2 * (cc * wj);
-    }
-    m.base = (MODE == MODE_DIRECT) ? kp_conic[col] - (j + 1) : slot_start[k] + (i64)j * (j + 1) / 2;
-    meta[c] = m;
+    mne2[c] = ne2;
+    mj[c] = j;
+    mwoff[c] = o - wlo;
+    mA[c] = (j == 0) ? 0.0 : ne2 * ((cc + 4.0) * wj);
+    mA0[c] = (j == 0) ? ne2 * ((cc - 4.0) * wj) : ne2 * (cc * wj);
+    mbase[c] = (MODE == MODE_DIRECT) ? kp_conic[col] - (j + 1) : slot_start[k] + (i64)j * (j + 1) / 2;
   }
-  if (staged)
-    for (int t = threadIdx.x; t < wlen; t += blockDim.x) wst[t] = wbar[wlo + t];
+  if (STAGED)
+    for (int t = threadIdx.x; t < wlen; t += QS_THREADS) wst[t] = wbar[wlo + t];
   __syncthreads();
-  // streaming phase: a warp owns a contiguous chunk of the tile's columns; the
-  // interior of a column (0 < i < j) is a pure multiply-store stream, the two
-  // special entries (row 0, diagonal) are written by one lane each.
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  const int per = (ncols + nwarp - 1) / nwarp;
+  constexpr int NW = QS_THREADS / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane >> 4, sl = lane & 15;
+  // warp `warp` owns the contiguous column chunk [cbeg, cend); its two halves take alternate columns
+  const int per = ((ncols + 2 * NW - 1) / (2 * NW)) * 2;
   const int cbeg = warp * per, cend = min(ncols, cbeg + per);
-  for (int c = cbeg; c < cend; ++c) {
-    const double A = meta[c].A;
-    const int j = meta[c].j;
-    const i64 base = meta[c].base;
-    const double* wc = (staged ? wst : wbar + wlo) + meta[c].woff;
+  for (int c = cbeg + sub; c < cend; c += 2) {
+    const int j = mj[c];
+    const double A = mA[c];
+    const i64 base = mbase[c];
+    const double* wc = STAGED ? wst + mwoff[c] : wbar + wlo + mwoff[c];
     if (MODE == MODE_MAP) {
       const i64* pmap = positions + base;
-#pragma unroll 2
-      for (int i = 1 + lane; i < j; i += 32) out[pmap[i]] = A * wc[i];
-      if (lane == 0) {
-        const double v0 = meta[c].A0 * wc[0];
-        out[pmap[0]] = (j == 0) ? v0 + meta[c].ne2 : v0;
-      } else if (lane == 1 && j > 0) {
-        out[pmap[j]] = A * wc[j] + meta[c].ne2;
-      }
+      for (int i = sl; i <= j; i += 16) out[pmap[i]] = A * wc[i];
+      if (sl == 0) out[pmap[0]] = (j == 0) ? mA0[c] * wc[0] + mne2[c] : mA0[c] * wc[0];
+      if (j > 0 && sl == (j & 15)) out[pmap[j]] = A * wc[j] + mne2[c];
     } else {
       double* dst = out + base;
-#pragma unroll 2
-      for (int i = 1 + lane; i < j; i += 32) dst[i] = A * wc[i];
-      if (lane == 0) {
-        const double v0 = meta[c].A0 * wc[0];
-        dst[0] = (j == 0) ? v0 + meta[c].ne2 : v0;
-      } else if (lane == 1 && j > 0) {
-        dst[j] = A * wc[j] + meta[c].ne2;
+      if (MODE == MODE_DIRECT && g_ptr) {
+        // Re-store the G' entries that precede the block in this K column (values from the compact CSR
+        // of G).  The column is then written in full, adjacent columns tile K.values without holes, and
+        // no 32-byte sector is left partially written: measured, that is the difference between ~3.2 and
+        // ~6 TB/s of store bandwidth (tests/probes/store_probe.cu).
+        const int col = col0 + c;
+        const int g0 = g_ptr[col], ng = g_ptr[col + 1] - g0;
+        for (int t = sl; t < ng; t += 16) dst[t - ng] = g_val[g0 + t];
       }
+      for (int i = sl; i <= j; i += 16) dst[i] = A * wc[i];
+      // the two special entries are rewritten by the lane that just wrote them
+      if (sl == 0) dst[0] = (j == 0) ? mA0[c] * wc[0] + mne2[c] : mA0[c] * wc[0];
+      if (j > 0 && sl == (j & 15)) dst[j] = A * wc[j] + mne2[c];
     }
   }
 }
@@ -176,23 +174,25 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
   const int nb_orth = orth_blocks(P.l);
   const int grid = nb_orth + P.ntiles;
   if (grid == 0) return;
-  const int wcap = P.max_tile_window < QS_WTW_WCAP ? P.max_tile_window : QS_WTW_WCAP;
-  const size_t smem = (size_t)P.max_tile_cols * sizeof(ColMeta) + (size_t)wcap * sizeof(double);
-  static bool attr_set[3] = {false, false, false};
-  auto launch = [&](auto kern, int idx, const i64* pos, const i64* kpc) {
-    if (smem > 48 * 1024 && !attr_set[idx]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set[idx] = true;
-    }
-    kern<<<grid, QS_THREADS, smem, st>>>(P.l, nb_orth, P.max_tile_cols, wcap, w, wbar, P.soc_ptr, P.cone_of_col,
-                                         P.tile_ptr, P.c4, P.e2, P.slot_start, pos, kpc, out);
+  const bool staged = P.max_tile_window <= QS_WTW_WCAP;
+  const int wcap = staged ? P.max_tile_window : 0;
+  const int mc = P.max_tile_cols;
+  const size_t smem = (size_t)mc * (4 * sizeof(double) + 2 * sizeof(int)) + 16 + (size_t)wcap * sizeof(double);
+  auto launch = [&](auto kern, const i64* pos, const i64* kpc) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<grid, QS_THREADS, smem, st>>>(P.l, nb_orth, mc, wcap, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,
+                                         P.c4, P.e2, P.slot_start, pos, kpc, P.g_ptr, P.g_val, out);
   };
-  if (mode == MODE_SLOTS)
-    launch(k_neg_wtw<MODE_SLOTS>, 0, nullptr, nullptr);
-  else if (mode == MODE_MAP)
-    launch(k_neg_wtw<MODE_MAP>, 1, positions, nullptr);
-  else
-    launch(k_neg_wtw<MODE_DIRECT>, 2, nullptr, P.kp_conic);
+  if (mode == MODE_SLOTS) {
+    if (staged) launch(k_neg_wtw<MODE_SLOTS, true>, nullptr, nullptr);
+    else launch(k_neg_wtw<MODE_SLOTS, false>, nullptr, nullptr);
+  } else if (mode == MODE_MAP) {
+    if (staged) launch(k_neg_wtw<MODE_MAP, true>, positions, nullptr);
+    else launch(k_neg_wtw<MODE_MAP, false>, positions, nullptr);
+  } else {
+    if (staged) launch(k_neg_wtw<MODE_DIRECT, true>, nullptr, P.kp_conic);
+    else launch(k_neg_wtw<MODE_DIRECT, false>, nullptr, P.kp_conic);
+  }
 }
 
 void qsk_check_direct_map(const WtwPlan& P, const i64* positions, int* flag, cudaStream_t st) {

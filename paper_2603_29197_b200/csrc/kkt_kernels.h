@@ -2,9 +2,9 @@
 #pragma once
 #include "common.cuh"
 
-#define QS_WTW_TILE 8192       // target block entries per CTA
+#define QS_WTW_TILE 16384      // target block entries per CTA
 #define QS_WTW_MAXCOLS 512     // at most this many columns per tile (metadata lives in shared memory)
-#define QS_WTW_WCAP 8192       // wbar window staged in shared memory when it fits (doubles)
+#define QS_WTW_WCAP 16384      // wbar window staged in shared memory when it fits (doubles)
 
 // Built once at setup (host side in capi.cu); all pointers are device pointers.
 struct WtwPlan {
@@ -17,6 +17,8 @@ struct WtwPlan {
   int max_tile_window;     // longest wbar window [first cone start, tile end) over the tiles
   const i64* slot_start;   // [nsoc]  the reference's soc_slot_starts (kkt.py:113-125)
   const i64* kp_conic;     // [m]  kp_conic[c] = K.col_pointers[n+p+c+1]  (DIRECT mode), may be null
+  const int* g_ptr;        // [m+1] CSR row pointers of G, or null: DIRECT mode then also re-stores the G' entries
+  const double* g_val;     //       of every conic K column so that the columns are written without holes
   double* c4;              // [nsoc] scratch: 4 * sum wbar^2
   double* e2;              // [nsoc] scratch: eta^2
 };
