@@ -153,6 +153,8 @@ int qs_initialize_iterate(qs_handle* h, double* mu_host);
 int qs_residuals(qs_handle* h, qs_residual_info* out);
 int qs_step(qs_handle* h, qs_step_info* out);
 int qs_get_iterate(qs_handle* h, double* x, double* y, double* z, double* s);
+/* Ruiz scalings D[n], E[p], F[m] (only when settings.ruiz_iters > 0; not a reference feature) */
+int qs_get_ruiz(qs_handle* h, double* D, double* E, double* F);
 int qs_set_iterate(qs_handle* h, const double* x, const double* y, const double* z, const double* s);
 int qs_get_scaling(qs_handle* h, double* w, double* eta, double* wbar, double* lam);
 /* load an NTScalingSet (cones.py:120-143) computed elsewhere; used by LinsysBackend.update(scaling) */

@@ -686,3 +686,48 @@ def solve(data, settings=None, perm=None, hook=None, trace=None) -> OracleResult
                         backend.n_factor, backend.n_solve,
                         dict(factor=backend.t_factor, linsolve=backend.t_solve, hot_path=t_hot,
                              analysis=backend.analysis_seconds, L_nnz=int(backend.sym.Li.size)))
+
+
+# ------------------------------------------------------------------- ruiz ----
+def ruiz_scalings(data, iters):
+    """NumPy restatement of the GPU path's Ruiz equilibration (csrc/ruiz_kernels.cu).
+
+    PARITY UNPINNED: the reference has no equilibration; this
+    follows upstream QOCO's scheme and only pins the CUDA kernels to a second,
+    independent implementation.  Returns (D, E, F) with the scaled problem
+    P^ = D P D, A^ = E A D, G^ = F G D, c^ = D c, b^ = E b, h^ = F h."""
+    import scipy.sparse as sp
+
+    def mat(M):
+        return sp.csc_matrix((M.values, M.row_indices, M.col_pointers), shape=(M.rows, M.cols))
+
+    n, p, m = data.n, data.p, data.m
+    Pu = mat(data.P)
+    P = (Pu + Pu.T - sp.diags(Pu.diagonal())).tocsr()
+    A, G = mat(data.A).tocsr(), mat(data.G).tocsr()
+    D, E, F = np.ones(n), np.ones(p), np.ones(m)
+    starts, dims = soc_layout(data.cone)
+
+    def rowmax(M):
+        M = abs(M).tocsr()
+        out = np.zeros(M.shape[0])
+        if M.nnz:
+            nz = np.diff(M.indptr) > 0
+            out[nz] = np.maximum.reduceat(M.data, M.indptr[:-1][nz])
+        return out
+
+    for _ in range(iters):
+        Ps = sp.diags(D) @ P @ sp.diags(D)
+        As = sp.diags(E) @ A @ sp.diags(D) if p else A
+        Gs = sp.diags(F) @ G @ sp.diags(D)
+        nx = np.maximum(rowmax(Ps), rowmax(Gs.T.tocsr()))
+        if p:
+            nx = np.maximum(nx, rowmax(As.T.tocsr()))
+        ny = rowmax(As) if p else np.zeros(0)
+        nz_ = rowmax(Gs)
+        for o, d in zip(starts.tolist(), dims.tolist()):
+            nz_[o:o + d] = nz_[o:o + d].max()
+        for sc, nr in ((D, nx), (E, ny), (F, nz_)):
+            pos = nr > 0
+            sc[pos] *= 1.0 / np.sqrt(nr[pos])
+    return D, E, F

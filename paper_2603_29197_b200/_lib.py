@@ -79,6 +79,7 @@ SIGNATURES = {
     "qs_step": (C.c_int, [vp, C.POINTER(QsStepInfo)]),
     "qs_get_iterate": (C.c_int, [vp] * 5),
     "qs_set_iterate": (C.c_int, [vp] * 5),
+    "qs_get_ruiz": (C.c_int, [vp] * 4),
     "qs_get_scaling": (C.c_int, [vp] * 5),
     "qs_set_scaling": (C.c_int, [vp] * 5),
     "qs_get_counters": (C.c_int, [vp, i64p, i64p, i64p]),

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17", "--extended-lambda",
               "-fmad=false",  # keep the reference's mul-then-add rounding (no FMA contraction)
               "-Xcompiler", "-fPIC"]
-CU = ["cone_kernels.cu", "kkt_kernels.cu", "spmv_kernels.cu", "ldl.cu", "capi.cu"]
+CU = ["cone_kernels.cu", "kkt_kernels.cu", "spmv_kernels.cu", "ruiz_kernels.cu", "ldl.cu", "capi.cu"]
 CPP = ["host_setup.cpp"]
 FMA_OK = {"ldl.cu"}  # the factorisation is not a restatement of reference arithmetic: let it use FMA
 

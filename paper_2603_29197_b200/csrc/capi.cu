@@ -11,6 +11,7 @@
 #include "host_setup.h"
 #include "kkt_kernels.h"
 #include "ldl.h"
+#include "ruiz_kernels.h"
 #include "spmv_kernels.h"
 
 namespace {
@@ -144,6 +145,8 @@ struct qs_handle {
   double *d = nullptr, *dcomp = nullptr, *wdz = nullptr, *ds = nullptr, *r_cone = nullptr, *w2vz = nullptr;
   double *rhs = nullptr, *sol = nullptr, *xa = nullptr, *xb = nullptr, *ra = nullptr, *rb = nullptr, *dx = nullptr;
   double* tmp_m = nullptr;
+  // Ruiz scalings (null when ruiz_iters == 0)
+  double *rD = nullptr, *rE = nullptr, *rF = nullptr;
 };
 
 namespace {
@@ -784,6 +787,26 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
 #undef ALLOC
   cudaMemsetAsync(h->wbar, 0, m * sizeof(double), st);
   h->sol = h->xa;
+  if (h->st.ruiz_iters > 0) {
+    std::vector<double> ones(std::max<i64>(std::max<i64>(n, p), m), 1.0);
+    h->rD = P.upload(ones.data(), n, st);
+    h->rE = P.upload(ones.data(), p, st);
+    h->rF = P.upload(ones.data(), m, st);
+    if (!h->rD || !h->rE || !h->rF) return fail(h, QS_E_MEMORY, "out of device memory for the Ruiz scalings");
+    RuizArgs R{(int)n, (int)p, (int)m, h->L.nsoc, h->L.soc_ptr, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->rD, h->rE, h->rF};
+    qsk_ruiz(R, (int)h->st.ruiz_iters, h->xa, h->xa + n, h->xa + n + p, st);
+    qsk_ruiz_apply(R, h->d_Kp, h->d_Ki, h->d_Kx, h->c, h->b, h->hv, st);
+    // norms of the scaled data feed the termination test
+    std::vector<double> hc(n), hb(p), hh(m);
+    CK(h, cudaMemcpyAsync(hc.data(), h->c, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaMemcpyAsync(hb.data(), h->b, p * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaMemcpyAsync(hh.data(), h->hv, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(h, cudaStreamSynchronize(st));
+    h->norm_c = inf_norm(hc.data(), n);
+    h->norm_b = inf_norm(hb.data(), p);
+    h->norm_h = inf_norm(hh.data(), m);
+    h->launches += 6 * h->st.ruiz_iters + 9;
+  }
   h->tm.total[T_H2D] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_h2d).count();
   // ---- factorisation analysis; the SOC blocks are cliques of the pattern
   std::vector<i64> cstart(nsoc), csize(nsoc);
@@ -986,10 +1009,37 @@ int qs_step(qs_handle* h, qs_step_info* out) {
 int qs_get_iterate(qs_handle* h, double* x, double* y, double* z, double* s) {
   NEED_PROBLEM(h)
   cudaStream_t st = h->stream;
-  if (x) CK(h, cudaMemcpyAsync(x, h->x, h->n * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (y) CK(h, cudaMemcpyAsync(y, h->y, h->p * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (z) CK(h, cudaMemcpyAsync(z, h->z, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (s) CK(h, cudaMemcpyAsync(s, h->s, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  const double *sx = h->x, *sy = h->y, *sz = h->z, *ss = h->s;
+  if (h->rD) {  // back to the caller's scaling: x = D x^, y = E y^, z = F z^, s = s^ / F
+    double* t = h->dx;  // scratch of length n + p + m
+    CK(h, cudaMemcpyAsync(t, h->x, h->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(h, cudaMemcpyAsync(t + h->n, h->y, h->p * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(h, cudaMemcpyAsync(t + h->n + h->p, h->z, h->m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(h, cudaMemcpyAsync(h->tmp_m, h->s, h->m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    qsk_vec_scale((int)h->n, t, h->rD, 0, st);
+    qsk_vec_scale((int)h->p, t + h->n, h->rE, 0, st);
+    qsk_vec_scale((int)h->m, t + h->n + h->p, h->rF, 0, st);
+    qsk_vec_scale((int)h->m, h->tmp_m, h->rF, 1, st);
+    sx = t;
+    sy = t + h->n;
+    sz = t + h->n + h->p;
+    ss = h->tmp_m;
+  }
+  if (x) CK(h, cudaMemcpyAsync(x, sx, h->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (y) CK(h, cudaMemcpyAsync(y, sy, h->p * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (z) CK(h, cudaMemcpyAsync(z, sz, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (s) CK(h, cudaMemcpyAsync(s, ss, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  return QS_OK;
+}
+
+int qs_get_ruiz(qs_handle* h, double* D, double* E, double* F) {
+  NEED_PROBLEM(h)
+  if (!h->rD) return fail(h, QS_E_INVALID, "ruiz_iters is 0: the problem is not equilibrated");
+  cudaStream_t st = h->stream;
+  if (D) CK(h, cudaMemcpyAsync(D, h->rD, h->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (E) CK(h, cudaMemcpyAsync(E, h->rE, h->p * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (F) CK(h, cudaMemcpyAsync(F, h->rF, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(h, cudaStreamSynchronize(st));
   return QS_OK;
 }

@@ -15,7 +15,7 @@
 typedef long long i64;
 
 #define QS_THREADS 256
-#define QS_MAX_GRID 4096  // every reducing kernel launches at most this many blocks
+#define QS_MAX_GRID 8192  // every reducing kernel launches at most this many blocks
 #define QS_RED_MAXK 16    // widest grid reduction (values per block)
 #define QS_UNBOUNDED DBL_MAX  // _cone_kernels.py:13
 

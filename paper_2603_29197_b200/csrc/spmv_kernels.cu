@@ -29,6 +29,46 @@ __device__ __forceinline__ double row_dot(const Csr& M, int row, const double* _
   return acc;
 }
 
+// Four rows at once with the same lane group: four independent load chains
+// (row pointer -> index/value -> x) are in flight per thread instead of one.
+// Rows are short here (1..50 entries), so the products are latency-bound and
+// memory-level parallelism is what buys bandwidth.
+__device__ __forceinline__ void row_dot4(const Csr& M, const int (&row)[4], const double* __restrict__ x, int lane,
+                                         int tpr, unsigned mask, double (&acc)[4]) {
+  int b[4], e[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const bool ok = row[r] < M.rows;
+    b[r] = ok ? M.ptr[row[r]] + lane : 0;
+    e[r] = ok ? M.ptr[row[r] + 1] : 0;
+    acc[r] = 0.0;
+  }
+  bool more = true;
+  while (more) {
+    more = false;
+    int ix[4];
+    double va[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const bool on = b[r] < e[r];
+      ix[r] = on ? M.idx[b[r]] : 0;
+      va[r] = on ? M.val[b[r]] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (b[r] < e[r]) {
+        acc[r] += va[r] * x[ix[r]];
+        b[r] += tpr;
+        more |= b[r] < e[r];
+      }
+    }
+  }
+  for (int o = tpr >> 1; o > 0; o >>= 1) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[r] += __shfl_xor_sync(mask, acc[r], o);
+  }
+}
+
 __device__ __forceinline__ unsigned lane_mask(int tpr) {
   return tpr == 32 ? 0xffffffffu : (((1u << tpr) - 1u) << (threadIdx.x & 31 & ~(tpr - 1)));
 }
@@ -79,43 +119,64 @@ __global__ void __launch_bounds__(QS_THREADS)
   for (int k = 0; k < NV; ++k) v[k] = 0.0;
   const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
   if (r.which == 0) {
-    for (int row = r.row; row < A.n; row += r.stride) {
-      const double px = row_dot(A.Pf, row, A.x, r.lane, r.tpr, r.mask);
-      const double aty = row_dot(A.At, row, A.y, r.lane, r.tpr, r.mask);
-      const double gtz = row_dot(A.Gt, row, A.z, r.lane, r.tpr, r.mask);
+    for (int row0 = r.row; row0 < A.n; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double px[4], aty[4], gtz[4];
+      row_dot4(A.Pf, rows, A.x, r.lane, r.tpr, r.mask, px);
+      row_dot4(A.At, rows, A.y, r.lane, r.tpr, r.mask, aty);
+      row_dot4(A.Gt, rows, A.z, r.lane, r.tpr, r.mask, gtz);
       if (r.lane == 0) {
-        const double ci = A.c[row], xi = A.x[row];
-        const double rd = px + ci + aty + gtz;  // ipm.py:76
-        A.rhs[row] = -rd;
-        v[PX] = absmax(v[PX], px);
-        v[ATY] = absmax(v[ATY], aty);
-        v[GTZ] = absmax(v[GTZ], gtz);
-        v[RD] = absmax(v[RD], rd);
-        v[XPX] += xi * px;
-        v[CX] += ci * xi;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = rows[q];
+          if (row >= A.n) continue;
+          const double ci = A.c[row], xi = A.x[row];
+          const double rd = px[q] + ci + aty[q] + gtz[q];  // ipm.py:76
+          A.rhs[row] = -rd;
+          v[PX] = absmax(v[PX], px[q]);
+          v[ATY] = absmax(v[ATY], aty[q]);
+          v[GTZ] = absmax(v[GTZ], gtz[q]);
+          v[RD] = absmax(v[RD], rd);
+          v[XPX] += xi * px[q];
+          v[CX] += ci * xi;
+        }
       }
     }
   } else if (r.which == 1) {
-    for (int row = r.row; row < A.p; row += r.stride) {
-      const double ax = row_dot(A.Ar, row, A.x, r.lane, r.tpr, r.mask);
+    for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double ax[4];
+      row_dot4(A.Ar, rows, A.x, r.lane, r.tpr, r.mask, ax);
       if (r.lane == 0) {
-        const double re = ax - A.b[row];  // ipm.py:77
-        A.rhs[A.n + row] = -re;
-        v[AX] = absmax(v[AX], ax);
-        v[RE] = absmax(v[RE], re);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = rows[q];
+          if (row >= A.p) continue;
+          const double re = ax[q] - A.b[row];  // ipm.py:77
+          A.rhs[A.n + row] = -re;
+          v[AX] = absmax(v[AX], ax[q]);
+          v[RE] = absmax(v[RE], re);
+        }
       }
     }
   } else {
-    for (int row = r.row; row < A.m; row += r.stride) {
-      const double gx = row_dot(A.Gr, row, A.x, r.lane, r.tpr, r.mask);
+    for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double gx[4];
+      row_dot4(A.Gr, rows, A.x, r.lane, r.tpr, r.mask, gx);
       if (r.lane == 0) {
-        const double si = A.s[row];
-        const double rc = gx + si - A.h[row];  // ipm.py:78
-        A.r_cone[row] = rc;
-        v[GX] = absmax(v[GX], gx);
-        v[SN] = absmax(v[SN], si);
-        v[RC] = absmax(v[RC], rc);
-        v[GAP] += si * A.z[row];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = rows[q];
+          if (row >= A.m) continue;
+          const double si = A.s[row];
+          const double rc = gx[q] + si - A.h[row];  // ipm.py:78
+          A.r_cone[row] = rc;
+          v[GX] = absmax(v[GX], gx[q]);
+          v[SN] = absmax(v[SN], si);
+          v[RC] = absmax(v[RC], rc);
+          v[GAP] += si * A.z[row];
+        }
       }
     }
   }
@@ -155,33 +216,51 @@ __global__ void __launch_bounds__(QS_THREADS)
   const double* vy = A.v + A.n;
   const double* vz = A.v + A.n + A.p;
   if (r.which == 0) {
-    for (int row = r.row; row < A.n; row += r.stride) {
-      const double px = row_dot(A.Pf, row, vx, r.lane, r.tpr, r.mask);
-      const double aty = row_dot(A.At, row, vy, r.lane, r.tpr, r.mask);
-      const double gtz = row_dot(A.Gt, row, vz, r.lane, r.tpr, r.mask);
+    for (int row0 = r.row; row0 < A.n; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double px[4], aty[4], gtz[4];
+      row_dot4(A.Pf, rows, vx, r.lane, r.tpr, r.mask, px);
+      row_dot4(A.At, rows, vy, r.lane, r.tpr, r.mask, aty);
+      row_dot4(A.Gt, rows, vz, r.lane, r.tpr, r.mask, gtz);
       if (r.lane == 0) {
-        const double t = A.rhs[row] - (px + aty + gtz);
-        A.r[row] = t;
-        v[0] = absmax(v[0], t);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (rows[q] >= A.n) continue;
+          const double t = A.rhs[rows[q]] - (px[q] + aty[q] + gtz[q]);
+          A.r[rows[q]] = t;
+          v[0] = absmax(v[0], t);
+        }
       }
     }
   } else if (r.which == 1) {
-    for (int row = r.row; row < A.p; row += r.stride) {
-      const double ax = row_dot(A.Ar, row, vx, r.lane, r.tpr, r.mask);
+    for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double ax[4];
+      row_dot4(A.Ar, rows, vx, r.lane, r.tpr, r.mask, ax);
       if (r.lane == 0) {
-        const double t = A.rhs[A.n + row] - ax;
-        A.r[A.n + row] = t;
-        v[0] = absmax(v[0], t);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (rows[q] >= A.p) continue;
+          const double t = A.rhs[A.n + rows[q]] - ax[q];
+          A.r[A.n + rows[q]] = t;
+          v[0] = absmax(v[0], t);
+        }
       }
     }
   } else {
-    for (int row = r.row; row < A.m; row += r.stride) {
-      const double gx = row_dot(A.Gr, row, vx, r.lane, r.tpr, r.mask);
+    for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double gx[4];
+      row_dot4(A.Gr, rows, vx, r.lane, r.tpr, r.mask, gx);
       if (r.lane == 0) {
-        const int i = A.n + A.p + row;
-        const double t = A.rhs[i] - (gx - A.w2vz[row]);
-        A.r[i] = t;
-        v[0] = absmax(v[0], t);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (rows[q] >= A.m) continue;
+          const int i = A.n + A.p + rows[q];
+          const double t = A.rhs[i] - (gx[q] - A.w2vz[rows[q]]);
+          A.r[i] = t;
+          v[0] = absmax(v[0], t);
+        }
       }
     }
   }
@@ -243,7 +322,8 @@ int blocks_for(int rows, int tpr) {
 }
 
 int blocks_capped(int rows, int tpr) {
-  const int b = blocks_for(rows, tpr), cap = QS_MAX_GRID / 4;
+  // a lane group takes 4 rows per trip; enough blocks that most groups make one trip
+  const int b = blocks_for((rows + 3) / 4, tpr), cap = QS_MAX_GRID / 4;
   return b > cap ? cap : b;
 }
 

@@ -129,6 +129,12 @@ class DeviceSolver:
         a = [None if v is None else _lib.f64(v) for v in (x, y, z, s)]
         self._check(self.lib.qs_set_iterate(self.h, *[_lib.ptr(v) for v in a]))
 
+    def ruiz_scalings(self):
+        d = self.data
+        D, E, F = np.empty(d.n), np.empty(d.p), np.empty(d.m)
+        self._check(self.lib.qs_get_ruiz(self.h, _lib.ptr(D), _lib.ptr(E), _lib.ptr(F)))
+        return D, E, F
+
     def scaling(self):
         from .cones import NTScalingSet
 
