@@ -1,0 +1,22 @@
+#!/bin/bash
+# One gpurun call: GPU parity tests, the bench line, the ncu launch list of the same bench command and one
+# `ncu --set full` capture of the dominant kernel.  Usage (from the repo root, on the GPU box):
+#   bash tools/gpu_round.sh <tag>
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,memory.total --format=csv > $OUT/gpu.txt 2>&1
+python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $OUT/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $OUT/smoke.log
+python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
+python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
+python tests/gpu_microbench.py > $OUT/microbench.txt 2>&1
+# launch list of the bench command (resident arm only: 1 warm-up solve + 1 timed solve)
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 1 --warmup 1 --no-cpu --e2e-steps 0 > $OUT/bench_under_ncu.log 2>&1
+# full capture of the dominant hot-path kernel (and the other cone kernels) on the C4 cone layout
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_neg_wtw|cone_kernel|k_residuals' -c 16 \
+    -o $OUT/hot_kernels -f python tests/gpu_microbench.py 10000 20 250 0 1 > $OUT/ncu_full.log 2>&1
+ls -la $OUT
+tail -3 $OUT/pytest_gpu.log; cat $OUT/bench.json | cut -c1-3000
