@@ -167,6 +167,9 @@ int qs_get_factor_stats(qs_handle* h, double* stats8);
 /* time `reps` launches of one hot-path kernel on the current state (CUDA events on the handle's stream);
  * kernel ids in INTEGRATION.md.  Returns mean milliseconds per launch. */
 int qs_time_kernel(qs_handle* h, int kernel_id, int reps, double* ms_host);
+/* same, but the L2 is flushed (256 MiB rewritten) before every timed launch and each launch is bracketed by its own
+ * pair of events: the cold-cache figure a kernel sees inside a solve */
+int qs_time_kernel_cold(qs_handle* h, int kernel_id, int reps, double* ms_host);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ SIGNATURES = {
     "qs_get_timers": (C.c_int, [vp, vp]),
     "qs_get_factor_stats": (C.c_int, [vp, vp]),
     "qs_time_kernel": (C.c_int, [vp, C.c_int, C.c_int, f64p]),
+    "qs_time_kernel_cold": (C.c_int, [vp, C.c_int, C.c_int, f64p]),
 }
 
 _lib = None

@@ -129,8 +129,7 @@ struct qs_handle {
   double norm_c = 0, norm_b = 0, norm_h = 0;
   // KKT
   i64 knnz = 0;
-  std::vector<i64> Kp_h, Ki_h, pos_h;
-  std::vector<double> Kx_h;
+  std::vector<i64> Kp_h;  // host copy of the KKT column pointers (the entries live on the device only)
   i64* d_Kp = nullptr;
   int* d_Ki = nullptr;
   double* d_Kx = nullptr;
@@ -473,12 +472,32 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   std::vector<int> ptr(nsoc + 1);
   std::vector<int> small_ids, big_ids;
   ptr[0] = (int)l;
+  // Lane-group width G from the mean size of the cones a warp could hold (dim <= 256): smallest power of two with
+  // 8 G >= mean.  A cone is "small" (lane group, whole cone in registers) iff dim <= G * R; the rest get a CTA.
+  double mean = 0.0;
+  i64 cnt = 0;
   for (i64 k = 0; k < nsoc; ++k) {
     if (q[k] < 1) return fail(h, QS_E_INVALID, "every SOC dimension must be >= 1");
+    if (q[k] <= 256) {
+      mean += (double)q[k];
+      ++cnt;
+    }
+  }
+  mean = cnt ? mean / cnt : 256.0;
+  int G = 1, single = -1;
+  while (G < 32 && G * 8 < mean) G <<= 1;
+  // experiment knobs (tests/gpu_cone_sweep.py): QS_CONE_G, QS_CONE_SINGLE
+  if (const char* e = getenv("QS_CONE_G")) {
+    G = 1;
+    while (G < 32 && G < atoi(e)) G <<= 1;
+  }
+  if (const char* e = getenv("QS_CONE_SINGLE")) single = atoi(e) != 0;
+  const i64 small_cap = std::min<i64>((i64)G * 8, big_threshold);
+  for (i64 k = 0; k < nsoc; ++k) {
     m += q[k];
     if (m >= ((i64)1 << 31)) return fail(h, QS_E_DIMENSION, "m exceeds 2^31");
     ptr[k + 1] = (int)m;
-    (q[k] > big_threshold ? big_ids : small_ids).push_back((int)k);
+    (q[k] > small_cap ? big_ids : small_ids).push_back((int)k);
   }
   h->q_host.assign(q, q + nsoc);
   h->soc_ptr_host = ptr;
@@ -491,15 +510,8 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   L.nbig = (int)big_ids.size();
   L.small_ids = big_ids.empty() ? nullptr : h->cone_pool.upload(small_ids.data(), small_ids.size(), h->stream);
   L.big_ids = big_ids.empty() ? nullptr : h->cone_pool.upload(big_ids.data(), big_ids.size(), h->stream);
-  // lanes per small cone: largest power of two <= mean small-cone size / 2, clamped to [1, 32]
-  double mean = 0.0;
-  for (int k : small_ids) mean += (double)q[k];
-  mean = small_ids.empty() ? 1.0 : mean / small_ids.size();
-  int G = 1;
-  double div = 4.0;
-  if (const char* e = getenv("QS_GROUP_DIV")) div = atof(e) > 0 ? atof(e) : div;  // tuning knob
-  while (G < 32 && G * div <= mean) G <<= 1;
   L.group = G;
+  L.single = single;
   h->deg = (double)(l + nsoc);
   // -W'W plan: column tiles of ~QS_WTW_TILE block entries
   WtwPlan& P = h->wp;
@@ -541,6 +553,28 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   P.kp_conic = nullptr;
   P.g_ptr = nullptr;
   P.g_val = nullptr;
+  // staged variant, dense-slot output: tiles of <= QS_WTW_STAGE packed slots
+  std::vector<int> st_ptr;  // outlives the stream synchronisation below
+  {
+    st_ptr.push_back((int)l);
+    i64 run = 0;
+    for (i64 k = 0; k < nsoc; ++k)
+      for (i64 j = 0; j < q[k]; ++j) {
+        if (run + j + 1 > QS_WTW_STAGE || ptr[k] + (int)j - st_ptr.back() >= QS_WTW_SCOLS) {
+          st_ptr.push_back(ptr[k] + (int)j);
+          run = 0;
+        }
+        run += j + 1;
+      }
+    if (st_ptr.back() != (int)m) st_ptr.push_back((int)m);
+    bool fits = true;  // a single column longer than the stage cannot be staged
+    for (i64 k = 0; k < nsoc; ++k) fits = fits && q[k] <= QS_WTW_STAGE;
+    P.n_stiles_slots = fits ? (int)st_ptr.size() - 1 : 0;
+    P.stile_ptr = fits ? h->cone_pool.upload(st_ptr.data(), st_ptr.size(), h->stream) : nullptr;
+    P.stile_ptr_direct = nullptr;
+    P.n_stiles_direct = 0;
+    P.kstart = nullptr;
+  }
   P.c4 = h->cone_pool.alloc<double>(nsoc);
   P.e2 = h->cone_pool.alloc<double>(nsoc);
   h->cone_tmp = h->cone_pool.alloc<double>(m);
@@ -724,18 +758,30 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
       }
     }
   }
-  // ---- KKT system (host), then to the device
+  // ---- KKT system: column pointers + compact pattern on the host (O(N + nnz(P,A,G))); the 10^8 entries
+  // themselves (row indices, initial values, slot -> position map) are written by the device (qsk_kkt_fill).
+  // QS_HOST_ASSEMBLY=1 keeps the original host assembly + upload as the checked alternative.
   KktDims dims{n, p, m, l, nsoc, (const i64*)q};
   h->knnz = hs_kkt_nnz(dims, (const i64*)Pp, (const i64*)Pi, nnzA, nnzG);
   if (h->knnz >= ((i64)1 << 31)) return fail(h, QS_E_DIMENSION, "KKT nonzeros exceed 2^31");
+  const bool host_assembly = getenv("QS_HOST_ASSEMBLY") != nullptr;
   h->Kp_h.resize(N + 1);
-  h->Ki_h.resize(h->knnz);
-  h->Kx_h.resize(h->knnz);
-  h->pos_h.resize(h->S);
-  std::vector<i64> soc_starts(nsoc), view_off(nsoc + 2);
-  hs_kkt_assemble(dims, (const i64*)Pp, (const i64*)Pi, Px, Arp.data(), Ari.data(), Arx.data(), Grp.data(),
-                  Gri.data(), Grx.data(), h->Kp_h.data(), h->Ki_h.data(), h->Kx_h.data(), h->pos_h.data(),
-                  view_off.data(), soc_starts.data());
+  std::vector<i64> Kcp, Kci;  // compact pattern for the analysis
+  std::vector<i64> Ki_full, pos_full;
+  std::vector<double> Kx_full;
+  if (host_assembly) {
+    Ki_full.resize(h->knnz);
+    Kx_full.resize(h->knnz);
+    pos_full.resize(h->S);
+    std::vector<i64> soc_starts(nsoc), view_off(nsoc + 2);
+    hs_kkt_assemble(dims, (const i64*)Pp, (const i64*)Pi, Px, Arp.data(), Ari.data(), Arx.data(), Grp.data(),
+                    Gri.data(), Grx.data(), h->Kp_h.data(), Ki_full.data(), Kx_full.data(), pos_full.data(),
+                    view_off.data(), soc_starts.data());
+  } else {
+    hs_kkt_pattern(dims, (const i64*)Pp, (const i64*)Pi, Arp.data(), Ari.data(), Grp.data(), Gri.data(),
+                   h->Kp_h.data(), &Kcp, &Kci);
+    if (h->Kp_h[N] != h->knnz) return fail(h, QS_E_INVALID, "internal: KKT column pointers disagree with the count");
+  }
   const auto t_h2d = std::chrono::steady_clock::now();
   bool ok = make_csr(h, &h->Pf, n, n, Pfp.data(), Pfi.data(), Pfx.data()) &&
             make_csr(h, &h->At, n, p, (const i64*)Ap, (const i64*)Ai, Ax) &&
@@ -752,19 +798,63 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   h->norm_c = inf_norm(c, n);
   h->norm_b = inf_norm(b, p);
   h->norm_h = inf_norm(hvec, m);
-  {
-    std::vector<int> ki32 = to_i32(h->Ki_h.data(), h->Ki_h.size());
-    h->d_Kp = h->prob_pool.upload(h->Kp_h.data(), h->Kp_h.size(), st);
+  h->d_Kp = h->prob_pool.upload(h->Kp_h.data(), h->Kp_h.size(), st);
+  if (host_assembly) {
+    std::vector<int> ki32 = to_i32(Ki_full.data(), Ki_full.size());
     h->d_Ki = h->prob_pool.upload(ki32.data(), ki32.size(), st);
-    h->d_Kx = h->prob_pool.upload(h->Kx_h.data(), h->Kx_h.size(), st);
-    h->d_pos = h->prob_pool.upload(h->pos_h.data(), h->pos_h.size(), st);
+    h->d_Kx = h->prob_pool.upload(Kx_full.data(), Kx_full.size(), st);
+    h->d_pos = h->prob_pool.upload(pos_full.data(), pos_full.size(), st);
     CK(h, cudaStreamSynchronize(st));
+  } else {
+    Csr Pu{};
+    if (!make_csr(h, &Pu, n, n, (const i64*)Pp, (const i64*)Pi, Px))  // CSC of upper(P) = CSR of its transpose
+      return fail(h, QS_E_MEMORY, "out of device memory for P");
+    h->d_Ki = h->prob_pool.alloc<int>(h->knnz);
+    h->d_Kx = h->prob_pool.alloc<double>(h->knnz);
+    h->d_pos = h->prob_pool.alloc<i64>(h->S);
+    if (h->d_Kp && h->d_Ki && h->d_Kx && h->d_pos) {
+      WtwPlan plan = h->wp;
+      plan.slot_start = h->d_slot_start;
+      qsk_kkt_fill(plan, (int)n, (int)p, Pu, h->Ar, h->Gr, h->d_Kp, h->d_Ki, h->d_Kx, h->d_pos, st);
+      h->launches++;
+      CK(h, cudaStreamSynchronize(st));
+    }
   }
   if (!h->c || !h->b || !h->hv || !h->d_Kp || !h->d_Ki || !h->d_Kx || !h->d_pos)
     return fail(h, QS_E_MEMORY, "out of device memory for the KKT system");
   h->wp.kp_conic = h->d_Kp + n + p + 1;
   h->wp.g_ptr = h->Gr.ptr;
   h->wp.g_val = h->Gr.val;
+  // staged variant, in-place output: tiles of whole conic K columns (G' entries + block entries) whose run
+  // [Kp[n+p+c0], Kp[n+p+c1]) fits the stage; only when every conic column is exactly that union
+  {
+    const i64* kp = h->Kp_h.data() + n + p;
+    bool whole = true;
+    std::vector<int> st_ptr;
+    st_ptr.push_back((int)l);
+    i64 run_begin = kp[l];
+    for (i64 k = 0; k < nsoc && whole; ++k) {
+      const i64 o = h->soc_ptr_host[k];
+      for (i64 j = 0; j < q[k]; ++j) {
+        const i64 c = o + j, len = kp[c + 1] - kp[c];
+        if (len != (Grp[c + 1] - Grp[c]) + j + 1 || len > QS_WTW_STAGE) {
+          whole = false;
+          break;
+        }
+        if (kp[c + 1] - run_begin > QS_WTW_STAGE || c - st_ptr.back() >= QS_WTW_SCOLS) {
+          st_ptr.push_back((int)c);
+          run_begin = kp[c];
+        }
+      }
+    }
+    if (st_ptr.back() != (int)m) st_ptr.push_back((int)m);
+    if (whole && nsoc > 0) {
+      h->wp.stile_ptr_direct = h->prob_pool.upload(st_ptr.data(), st_ptr.size(), st);
+      h->wp.n_stiles_direct = (int)st_ptr.size() - 1;
+      h->wp.kstart = h->d_Kp + n + p;
+      CK(h, cudaStreamSynchronize(st));
+    }
+  }
   // closed-form map == explicit map?
   {
     int* flag = h->prob_pool.alloc<int>(1);
@@ -814,7 +904,9 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
     cstart[k] = n + p + h->soc_ptr_host[k];
     csize[k] = q[k];
   }
-  std::string err = h->ls.analyze(N, h->Kp_h.data(), h->Ki_h.data(), h->d_Kp, h->d_Ki, (int)h->st.ordering,
+  const i64* an_p = host_assembly ? h->Kp_h.data() : Kcp.data();
+  const i64* an_i = host_assembly ? Ki_full.data() : Kci.data();
+  std::string err = h->ls.analyze(N, an_p, an_i, h->knnz, h->d_Kp, h->d_Ki, (int)h->st.ordering,
                                   (const i64*)user_perm, nsoc, cstart.data(), csize.data(), n, h->st.static_reg, st);
   if (!err.empty()) return fail(h, err.find("memory") != std::string::npos ? QS_E_MEMORY : QS_E_INVALID, err);
   h->tm.total[T_ANALYSIS] += h->ls.analysis_seconds;
@@ -837,8 +929,16 @@ int64_t qs_kkt_size(qs_handle* h, int64_t* nnz, int64_t* slots) {
 int qs_get_kkt(qs_handle* h, int64_t* Kp, int64_t* Ki, double* Kx, int64_t* positions) {
   NEED_PROBLEM(h)
   if (Kp) memcpy(Kp, h->Kp_h.data(), h->Kp_h.size() * sizeof(i64));
-  if (Ki) memcpy(Ki, h->Ki_h.data(), h->Ki_h.size() * sizeof(i64));
-  if (positions) memcpy(positions, h->pos_h.data(), h->pos_h.size() * sizeof(i64));
+  if (Ki) {  // the device keeps int32 row indices; the reference contract is int64
+    std::vector<int> ki32(h->knnz);
+    CK(h, cudaMemcpyAsync(ki32.data(), h->d_Ki, h->knnz * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    for (i64 k = 0; k < h->knnz; ++k) Ki[k] = ki32[k];
+  }
+  if (positions) {
+    CK(h, cudaMemcpyAsync(positions, h->d_pos, h->S * sizeof(i64), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
   if (Kx) {  // current device values
     CK(h, cudaMemcpyAsync(Kx, h->d_Kx, h->knnz * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
@@ -1108,7 +1208,17 @@ int qs_get_factor_stats(qs_handle* h, double* s8) {
   return QS_OK;
 }
 
+static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, double* ms_host);
+
 int qs_time_kernel(qs_handle* h, int kernel_id, int reps, double* ms_host) {
+  return time_kernel_impl(h, kernel_id, reps, 0, ms_host);
+}
+
+int qs_time_kernel_cold(qs_handle* h, int kernel_id, int reps, double* ms_host) {
+  return time_kernel_impl(h, kernel_id, reps, 1, ms_host);
+}
+
+static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, double* ms_host) {
   NEED_PROBLEM(h)
   if (reps < 1) reps = 1;
   cudaStream_t st = h->stream;
@@ -1151,12 +1261,34 @@ int qs_time_kernel(qs_handle* h, int kernel_id, int reps, double* ms_host) {
   };
   if (kernel_id < 0 || kernel_id > 14) return fail(h, QS_E_INVALID, "unknown kernel id");
   run();  // warm-up
-  CK(h, cudaEventRecord(a, st));
-  for (int r = 0; r < reps; ++r) run();
-  CK(h, cudaEventRecord(b, st));
-  CK(h, cudaEventSynchronize(b));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
+  if (!cold) {
+    CK(h, cudaEventRecord(a, st));
+    for (int r = 0; r < reps; ++r) run();
+    CK(h, cudaEventRecord(b, st));
+    CK(h, cudaEventSynchronize(b));
+    cudaEventElapsedTime(&ms, a, b);
+  } else {
+    // cold: every timed launch starts with an L2 that holds none of its operands (256 MiB > 126 MB L2 rewritten
+    // in between), as inside a solve, where a 5.7 GB factorisation runs between two cone phases
+    const size_t flush_bytes = (size_t)256 << 20;
+    void* flush = nullptr;
+    if (cudaMalloc(&flush, flush_bytes) != cudaSuccess) return fail(h, QS_E_MEMORY, "L2 flush buffer");
+    cudaMemsetAsync(flush, 0, flush_bytes, st);
+    for (int r = 0; r < reps; ++r) {
+      // read-only sweep: the L2 ends up full of CLEAN lines of the flush buffer (a memset would leave dirty lines
+      // whose write-back would be billed to the timed kernel)
+      qsk_absmax((i64)(flush_bytes / sizeof(double)), (const double*)flush, h->scalars + SC_TMP2, nullptr, h->gr, st);
+      cudaEventRecord(a, st);
+      run();
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float one = 0.f;
+      cudaEventElapsedTime(&one, a, b);
+      ms += one;
+    }
+    cudaFree(flush);
+  }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   if (ms_host) *ms_host = (double)ms / reps;

@@ -66,6 +66,7 @@ struct ConeLayout {
   int m, l, nsoc;
   const int* soc_ptr;    // [nsoc+1]
   int group;             // lanes cooperating on one small cone (1,2,4,...,32)
+  int single;            // -1: each op picks its own decomposition; 0 / 1 force chunked / register-resident
   int nsmall;            // cones handled by lane groups
   const int* small_ids;  // [nsmall] or nullptr when every cone is small
   int nbig;              // cones handled by a whole CTA (dim > big threshold)
@@ -75,9 +76,14 @@ struct ConeLayout {
 // ------------------------------------------------------------ group policies
 // A "group" is the set of threads that cooperates on one cone.  sum() is an
 // all-reduce: every thread of the group gets the same bits back.
-template <int G>
+// kR = elements of the cone a thread keeps in registers per chunk; kSingle = the
+// whole cone is one chunk (group * kR >= dim by construction of the layout), so
+// multi-pass ops read HBM once and never touch memory again between passes.
+template <int G, int R_ = 4, bool SINGLE_ = false>
 struct LaneGroup {
   static constexpr int kSize = G;
+  static constexpr int kR = R_;
+  static constexpr bool kSingle = SINGLE_;
   __device__ __forceinline__ int lane() const { return threadIdx.x & (G - 1); }
   __device__ __forceinline__ int size() const { return G; }
   // shuffles name only this group's lanes, so groups of one warp may diverge
@@ -126,6 +132,8 @@ struct LaneGroup {
 };
 
 struct CtaGroup {
+  static constexpr int kR = 8;  // 256 threads x 8: cones up to 2048 stay in registers; longer ones are chunked
+  static constexpr bool kSingle = false;
   double* scratch;  // [32 * 4] shared
   __device__ __forceinline__ int lane() const { return threadIdx.x; }
   __device__ __forceinline__ int size() const { return blockDim.x; }
@@ -171,6 +179,25 @@ struct CtaGroup {
     sum4(a, b, c, d);
   }
 };
+
+// ------------------------------------------------------------ cone fragments
+// Slot r of a thread's fragment holds tail element t = base + lane + r * size of
+// the cone (head t = 0 excluded: it is handled by scalar code), zero when t is
+// outside [1, q).  All kR loads of a fragment are independent, so a thread has
+// kR x (number of vectors) loads in flight before the first use.
+#define QS_CHUNKS(base) for (int base = 0; base < (Grp::kSingle ? 1 : q); base += g.size() * Grp::kR)
+#define QS_FRAG(r, t) _Pragma("unroll") for (int r = 0, t = base + g.lane(); r < Grp::kR; ++r, t += g.size())
+#define QS_TAIL_OK(t, q) ((t) >= 1 && (t) < (q))
+
+template <class Grp>
+__device__ __forceinline__ void qs_frag_load(const Grp& g, const double* __restrict__ p, int q, int base,
+                                             double (&f)[Grp::kR]) {
+#pragma unroll
+  for (int r = 0; r < Grp::kR; ++r) {
+    const int t = base + g.lane() + r * g.size();
+    f[r] = QS_TAIL_OK(t, q) ? p[t] : 0.0;
+  }
+}
 
 // ------------------------------------------------------- grid-wide reduction
 // Deterministic (fixed grid -> fixed order) reduction of K doubles across the

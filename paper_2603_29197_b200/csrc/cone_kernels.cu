@@ -6,10 +6,12 @@
 // ranges: [orthant | small SOCs | big SOCs].
 //   * orthant: grid-stride elementwise, 128-bit (double2) accesses;
 //   * small SOCs: a power-of-two lane group (1..32 lanes, chosen from the mean
-//     cone size at setup) per cone, segmented reductions by xor-shuffles;
-//   * big SOCs (dim > threshold): one CTA per cone, shuffles + a shared-memory
-//     stage.
-// A cone is read once from HBM; later passes over the same cone hit L1/L2.
+//     cone size at setup) per cone, segmented reductions by xor-shuffles; the
+//     group keeps the whole cone in registers (R = 4 or 8 elements per lane,
+//     every load issued before the first use), so a multi-pass op reads HBM
+//     exactly once and its later passes touch no memory;
+//   * big SOCs (dim > group * R): one CTA per cone, shuffles + a shared-memory
+//     stage, registers up to dim 2048, chunked re-reads beyond that.
 //
 // Every op cites the reference lines whose arithmetic it reproduces
 // (paths relative to /root/reference/pkg/src/qsocp/).
@@ -20,8 +22,8 @@ namespace {
 // ------------------------------------------------------------------ dispatch
 struct NoAcc {};
 
-template <int G, class Op>
-__global__ void __launch_bounds__(QS_THREADS) cone_kernel(ConeLayout L, Op op, int nb_orth, int nb_small, int nb_big) {
+template <int G, int R, bool SINGLE, class Op>
+__global__ void __launch_bounds__(QS_THREADS, SINGLE ? 2 : 3) cone_kernel(ConeLayout L, Op op, int nb_orth, int nb_small, int nb_big) {
   typename Op::Acc acc;
   op.init(acc);
   const int b = blockIdx.x;
@@ -31,7 +33,7 @@ __global__ void __launch_bounds__(QS_THREADS) cone_kernel(ConeLayout L, Op op, i
     // lane groups stride over the small cones; groups of one warp may diverge
     // (their shuffles name only their own lanes)
     const int ngroups = nb_small * (QS_THREADS / G);
-    LaneGroup<G> g;
+    LaneGroup<G, R, SINGLE> g;
     for (int gid = ((b - nb_orth) * blockDim.x + threadIdx.x) / G; gid < L.nsmall; gid += ngroups) {
       const int k = L.small_ids ? L.small_ids[gid] : gid;
       const int o = L.soc_ptr[k];
@@ -65,14 +67,29 @@ void launch(const ConeLayout& L, const Op& op, cudaStream_t st) {
   const int nb_big = L.nbig > cap ? cap : L.nbig;
   const int grid = nb_orth + nb_small + nb_big;
   if (grid == 0) return;
+  // Two decompositions per lane-group width G (every small cone has dim <= 8 G, see qs_set_cones):
+  //   resident <G, 8, true>  the whole cone sits in registers, later passes touch no memory: best for the fused
+  //                          ops that combine 4-5 vectors (RhsConeOp, PostSolveOp, DcompOp);
+  //   chunked  <G, 4, false> 4 independent loads per vector per trip, later passes re-read L1/L2: fewer registers,
+  //                          more warps per SM; best for the 1-2 vector ops (measured: tests/gpu_cone_sweep.py).
+#define QS_LAUNCH(GG, RR, SS) \
+  cone_kernel<GG, RR, SS, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big)
+#define QS_CASE(GG)                                                                  \
+  case GG:                                                                           \
+    if (resident) QS_LAUNCH(GG, 8, true); else QS_LAUNCH(GG, 4, false);              \
+    break;
+  const bool resident = L.single >= 0 ? L.single != 0 : Op::kResident;
   switch (G) {
-    case 1: cone_kernel<1, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
-    case 2: cone_kernel<2, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
-    case 4: cone_kernel<4, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
-    case 8: cone_kernel<8, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
-    case 16: cone_kernel<16, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
-    default: cone_kernel<32, Op><<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, nb_small, nb_big); break;
+    QS_CASE(1)
+    QS_CASE(2)
+    QS_CASE(4)
+    QS_CASE(8)
+    QS_CASE(16)
+    default:
+    QS_CASE(32)
   }
+#undef QS_CASE
+#undef QS_LAUNCH
 }
 
 #define QS_EMPTY_GUARD(L) ((L).l == 0 && (L).nsoc == 0)
@@ -91,6 +108,7 @@ __device__ __forceinline__ double w_tail(double scale, double sgn, double wbt, d
 // compute_nt_scaling (cones.py:159-184) + soc_nt_scaling (_cone_kernels.py:16-53)
 // fused with lam o lam (ipm.py:191, _cone_kernels.py:77-89).
 struct NtScalingOp {
+  static constexpr bool kResident = false;
   const double* s;
   const double* z;
   double* w;
@@ -132,12 +150,19 @@ struct NtScalingOp {
   template <class Grp>
   __device__ void soc(Acc& a, const Grp& g, int k, int o, int q) const {
     const double s0 = q ? s[o] : 1.0, z0 = q ? z[o] : 1.0;
+    const double* sp = s + o;
+    const double* zp = z + o;
+    double sf[Grp::kR], zf[Grp::kR];
     double ss = 0.0, zz = 0.0, sz = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double a1 = s[o + t], b1 = z[o + t];
-      ss += a1 * a1;
-      zz += b1 * b1;
-      sz += a1 * b1;
+    QS_CHUNKS(base) {
+      qs_frag_load(g, sp, q, base, sf);
+      qs_frag_load(g, zp, q, base, zf);
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) {
+        ss += sf[r] * sf[r];
+        zz += zf[r] * zf[r];
+        sz += sf[r] * zf[r];
+      }
     }
     g.sum3(ss, zz, sz);
     const double sres = s0 * s0 - ss, zres = z0 * z0 - zz;
@@ -157,22 +182,34 @@ struct NtScalingOp {
     // and takes four fp64 divisions per element off the critical path
     const double isa = 1.0 / sa, iza = 1.0 / za, ik = 1.0 / ((2.0 * gamma) * den);
     double wz = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double zt = z[o + t];
-      const double wbt = (s[o + t] * isa - zt * iza) * ik;
-      wbar[o + t] = wbt;
-      wz += wbt * zt;
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, sp, q, base, sf);
+        qs_frag_load(g, zp, q, base, zf);
+      }
+      QS_FRAG(r, t) {
+        const double wbt = (sf[r] * isa - zf[r] * iza) * ik;
+        if (QS_TAIL_OK(t, q)) wbar[o + t] = wbt;
+        wz += wbt * zf[r];
+      }
     }
     wz = g.sum(wz) + wb0 * z0;
     const double lam0 = ek * (2.0 * wb0 * wz - z0);
     double ll = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double zt = z[o + t];
-      const double wbt = (s[o + t] * isa - zt * iza) * ik;
-      const double lt = ek * (2.0 * wbt * wz + zt);
-      lam[o + t] = lt;
-      ll += lt * lt;
-      if (lam_sq) lam_sq[o + t] = lam0 * lt + lam0 * lt;
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, sp, q, base, sf);
+        qs_frag_load(g, zp, q, base, zf);
+      }
+      QS_FRAG(r, t) {
+        const double wbt = (sf[r] * isa - zf[r] * iza) * ik;
+        const double lt = ek * (2.0 * wbt * wz + zf[r]);
+        ll += lt * lt;
+        if (QS_TAIL_OK(t, q)) {
+          lam[o + t] = lt;
+          if (lam_sq) lam_sq[o + t] = lam0 * lt + lam0 * lt;
+        }
+      }
     }
     ll = g.sum(ll);
     if (g.lane() == 0 && q) {
@@ -190,6 +227,7 @@ struct NtScalingOp {
 // -------------------------------------------------------------- apply W / W^-1
 // apply_scaling (cones.py:192-212) + soc_apply_w (_cone_kernels.py:56-74)
 struct ApplyWOp {
+  static constexpr bool kResident = false;
   const double* w;
   const double* eta;
   const double* wbar;
@@ -204,13 +242,27 @@ struct ApplyWOp {
   template <class Grp>
   __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
     const double sgn = inverse ? -1.0 : 1.0;
-    double dot = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) dot += sgn * wbar[o + t] * u[o + t];
     const double wb0 = q ? wbar[o] : 0.0, u0 = q ? u[o] : 0.0;
-    dot = wb0 * u0 + g.sum(dot);
     const double e = q ? eta[k] : 1.0;
+    double wf[Grp::kR], uf[Grp::kR];
+    double dot = 0.0;
+    QS_CHUNKS(base) {
+      qs_frag_load(g, wbar + o, q, base, wf);
+      qs_frag_load(g, u + o, q, base, uf);
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) dot += sgn * wf[r] * uf[r];
+    }
+    dot = wb0 * u0 + g.sum(dot);
     const double scale = inverse ? 1.0 / e : e;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = w_tail(scale, sgn, wbar[o + t], dot, u[o + t]);
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, u + o, q, base, uf);
+      }
+      QS_FRAG(r, t) {
+        if (QS_TAIL_OK(t, q)) out[o + t] = w_tail(scale, sgn, wf[r], dot, uf[r]);
+      }
+    }
     if (g.lane() == 0 && q) out[o] = w_head(scale, wb0, dot, u0);
   }
   __device__ void finish(Acc&) const {}
@@ -219,6 +271,7 @@ struct ApplyWOp {
 // ------------------------------------------------------------- Jordan product
 // jordan_product (cones.py:215-228) + soc_jordan (_cone_kernels.py:77-89)
 struct JordanProductOp {
+  static constexpr bool kResident = false;
   const double* u;
   const double* v;
   double* out;
@@ -231,10 +284,14 @@ struct JordanProductOp {
   __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
     const double u0 = q ? u[o] : 0.0, v0 = q ? v[o] : 0.0;
     double dot = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double ut = u[o + t], vt = v[o + t];
-      dot += ut * vt;
-      out[o + t] = u0 * vt + v0 * ut;
+    double uf[Grp::kR], vf[Grp::kR];
+    QS_CHUNKS(base) {
+      qs_frag_load(g, u + o, q, base, uf);
+      qs_frag_load(g, v + o, q, base, vf);
+      QS_FRAG(r, t) {
+        dot += uf[r] * vf[r];
+        if (QS_TAIL_OK(t, q)) out[o + t] = u0 * vf[r] + v0 * uf[r];
+      }
     }
     dot = u0 * v0 + g.sum(dot);
     if (g.lane() == 0 && q) out[o] = dot;
@@ -245,6 +302,7 @@ struct JordanProductOp {
 // ------------------------------------------------------------ Jordan division
 // jordan_divide (cones.py:231-244) + soc_jordan_div (_cone_kernels.py:92-106)
 struct JordanDivideOp {
+  static constexpr bool kResident = false;
   const double* lam;
   const double* v;
   double* out;
@@ -257,14 +315,27 @@ struct JordanDivideOp {
   __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
     const double a = q ? lam[o] : 1.0, v0 = q ? v[o] : 0.0;
     double ll = 0.0, cross = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double lt = lam[o + t];
-      ll += lt * lt;
-      cross += lt * v[o + t];
+    double lf[Grp::kR], vf[Grp::kR];
+    QS_CHUNKS(base) {
+      qs_frag_load(g, lam + o, q, base, lf);
+      qs_frag_load(g, v + o, q, base, vf);
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) {
+        ll += lf[r] * lf[r];
+        cross += lf[r] * vf[r];
+      }
     }
     g.sum2(ll, cross);
     const double u0 = (a * v0 - cross) / (a * a - ll);
-    for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = (v[o + t] - u0 * lam[o + t]) / a;
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, lam + o, q, base, lf);
+        qs_frag_load(g, v + o, q, base, vf);
+      }
+      QS_FRAG(r, t) {
+        if (QS_TAIL_OK(t, q)) out[o + t] = (vf[r] - u0 * lf[r]) / a;
+      }
+    }
     if (g.lane() == 0 && q) out[o] = u0;
   }
   __device__ void finish(Acc&) const {}
@@ -275,6 +346,7 @@ struct JordanDivideOp {
 // (cones.py:275-299), soc_max_step (_cone_kernels.py:109-146), soc_violation
 // (_cone_kernels.py:149-162).  Writes scalars[slot_step] and scalars[slot_viol].
 struct MaxStepOp {
+  static constexpr bool kResident = false;
   const double* u;
   const double* du;  // may be null: violation only
   double* scalars;
@@ -300,13 +372,17 @@ struct MaxStepOp {
   template <class Grp>
   __device__ void soc(Acc& acc, const Grp& g, int k, int o, int q) const {
     double uu = 0.0, dd = 0.0, ud = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double ut = u[o + t];
-      uu += ut * ut;
-      if (du) {
-        const double dt = du[o + t];
-        dd += dt * dt;
-        ud += ut * dt;
+    double uf[Grp::kR], df[Grp::kR];
+    QS_CHUNKS(base) {
+      qs_frag_load(g, u + o, q, base, uf);
+      if (du) qs_frag_load(g, du + o, q, base, df);
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) {
+        uu += uf[r] * uf[r];
+        if (du) {
+          dd += df[r] * df[r];
+          ud += uf[r] * df[r];
+        }
       }
     }
     g.sum3(uu, dd, ud);
@@ -336,6 +412,7 @@ struct MaxStepOp {
 // violation alpha = scalars[slot] is >= 0).  scale = -1 negates u first (the
 // initial slack is -z~, ipm.py:146).
 struct ShiftOp {
+  static constexpr bool kResident = false;
   const double* u;
   double* out;
   const double* scalars;
@@ -356,7 +433,13 @@ struct ShiftOp {
     const double alpha = scalars[slot];
     const double add = 1.0 + alpha;
     // tail: u + (1+alpha)*0.0 == u
-    for (int t = 1 + g.lane(); t < q; t += g.size()) out[o + t] = scale * u[o + t];
+    double uf[Grp::kR];
+    QS_CHUNKS(base) {
+      qs_frag_load(g, u + o, q, base, uf);
+      QS_FRAG(r, t) {
+        if (QS_TAIL_OK(t, q)) out[o + t] = scale * uf[r];
+      }
+    }
     if (g.lane() == 0 && q) {
       const double v = scale * u[o];
       out[o] = (alpha < 0.0) ? v : v + add;
@@ -368,6 +451,7 @@ struct ShiftOp {
 // ------------------------------------------------- corrector complementarity
 // d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a)   (ipm.py:209-211)
 struct DcompOp {
+  static constexpr bool kResident = true;
   const double* w;
   const double* eta;
   const double* wbar;
@@ -391,15 +475,35 @@ struct DcompOp {
     const double wb0 = q ? wbar[o] : 0.0, u0 = q ? ds_a[o] : 0.0, y0 = q ? wdz_a[o] : 0.0;
     const double scale = q ? 1.0 / eta[k] : 1.0;
     double dot = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) dot += -1.0 * wbar[o + t] * ds_a[o + t];
+    double wf[Grp::kR], af[Grp::kR], yf[Grp::kR], qf[Grp::kR];
+    QS_CHUNKS(base) {
+      qs_frag_load(g, wbar + o, q, base, wf);
+      qs_frag_load(g, ds_a + o, q, base, af);
+      if (Grp::kSingle) {  // second-pass operands: issue their loads now, they land during the reduction
+        qs_frag_load(g, wdz_a + o, q, base, yf);
+        qs_frag_load(g, lam_sq + o, q, base, qf);
+      }
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) dot += -1.0 * wf[r] * af[r];
+    }
     dot = wb0 * u0 + g.sum(dot);
     const double x0 = w_head(scale, wb0, dot, u0);  // (W^-1 ds_a)_0
     double cr = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double xt = w_tail(scale, -1.0, wbar[o + t], dot, ds_a[o + t]);
-      const double yt = wdz_a[o + t];
-      cr += xt * yt;
-      dcomp[o + t] = 0.0 - lam_sq[o + t] - (x0 * yt + y0 * xt);
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, ds_a + o, q, base, af);
+        qs_frag_load(g, wdz_a + o, q, base, yf);
+        qs_frag_load(g, lam_sq + o, q, base, qf);
+      }
+      QS_FRAG(r, t) {
+        const double xt = w_tail(scale, -1.0, wf[r], dot, af[r]);
+        const double yt = yf[r];
+        if (QS_TAIL_OK(t, q)) {
+          cr += xt * yt;
+          dcomp[o + t] = 0.0 - qf[r] - (x0 * yt + y0 * xt);
+        }
+      }
     }
     cr = x0 * y0 + g.sum(cr);
     if (g.lane() == 0 && q) dcomp[o] = sm - lam_sq[o] - cr;
@@ -410,6 +514,7 @@ struct DcompOp {
 // --------------------------------------------------- third RHS block (a-11)
 // d = lam \ (sign * dc) ; rhs_z = -r_cone - W d          (ipm.py:180-184)
 struct RhsConeOp {
+  static constexpr bool kResident = true;
   const double* w;
   const double* eta;
   const double* wbar;
@@ -432,26 +537,50 @@ struct RhsConeOp {
   __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
     const double a = q ? lam[o] : 1.0, v0 = q ? sign * dc[o] : 0.0;
     double ll = 0.0, cross = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double lt = lam[o + t];
-      ll += lt * lt;
-      cross += lt * (sign * dc[o + t]);
+    double lf[Grp::kR], cf[Grp::kR], wf[Grp::kR], rf[Grp::kR];
+    const double wb0 = q ? wbar[o] : 0.0;
+    const double e = q ? eta[k] : 1.0;
+    QS_CHUNKS(base) {
+      qs_frag_load(g, lam + o, q, base, lf);
+      qs_frag_load(g, dc + o, q, base, cf);
+      if (Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, r_cone + o, q, base, rf);
+      }
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) {
+        ll += lf[r] * lf[r];
+        cross += lf[r] * (sign * cf[r]);
+      }
     }
     g.sum2(ll, cross);
     const double d0 = (a * v0 - cross) / (a * a - ll);
     const double ia = 1.0 / a;
-    const double wb0 = q ? wbar[o] : 0.0;
     double dot = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) * ia;
-      d[o + t] = dt;
-      dot += wbar[o + t] * dt;
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, lam + o, q, base, lf);
+        qs_frag_load(g, dc + o, q, base, cf);
+        qs_frag_load(g, wbar + o, q, base, wf);
+      }
+      QS_FRAG(r, t) {
+        const double dt = (sign * cf[r] - d0 * lf[r]) * ia;
+        if (QS_TAIL_OK(t, q)) d[o + t] = dt;
+        dot += wf[r] * dt;
+      }
     }
     dot = wb0 * d0 + g.sum(dot);
-    const double e = q ? eta[k] : 1.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double dt = (sign * dc[o + t] - d0 * lam[o + t]) * ia;
-      rhs_z[o + t] = -r_cone[o + t] - w_tail(e, 1.0, wbar[o + t], dot, dt);
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, lam + o, q, base, lf);
+        qs_frag_load(g, dc + o, q, base, cf);
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, r_cone + o, q, base, rf);
+      }
+      QS_FRAG(r, t) {
+        const double dt = (sign * cf[r] - d0 * lf[r]) * ia;
+        if (QS_TAIL_OK(t, q)) rhs_z[o + t] = -rf[r] - w_tail(e, 1.0, wf[r], dot, dt);
+      }
     }
     if (g.lane() == 0 && q) {
       d[o] = d0;
@@ -467,6 +596,7 @@ struct RhsConeOp {
 // final:  predictor  alpha_aff = min(1, step_s, step_z)        (ipm.py:197)
 //         corrector  alpha = min(1, step_fraction * min(..))   (ipm.py:216-218)
 struct PostSolveOp {
+  static constexpr bool kResident = true;
   const double* w;
   const double* eta;
   const double* wbar;
@@ -507,41 +637,86 @@ struct PostSolveOp {
     const double dz0 = q ? dz[o] : 0.0, z0 = q ? z[o] : 1.0, s0 = q ? s[o] : 1.0, d0 = q ? d[o] : 0.0;
     // pass 1: w.dz and the (z, dz) quadratic
     double dot1 = 0.0, zz = 0.0, dd = 0.0, zd = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double dzt = dz[o + t], zt = z[o + t];
-      dot1 += wbar[o + t] * dzt;
-      zz += zt * zt;
-      dd += dzt * dzt;
-      zd += zt * dzt;
+    double wf[Grp::kR], gf[Grp::kR], df[Grp::kR], xf[Grp::kR];  // wbar, dz, d, and z (pass 1) then s (pass 3)
+    QS_CHUNKS(base) {
+      qs_frag_load(g, wbar + o, q, base, wf);
+      qs_frag_load(g, dz + o, q, base, gf);
+      qs_frag_load(g, z + o, q, base, xf);
+      if (Grp::kSingle) qs_frag_load(g, d + o, q, base, df);
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) {
+        dot1 += wf[r] * gf[r];
+        zz += xf[r] * xf[r];
+        dd += gf[r] * gf[r];
+        zd += xf[r] * gf[r];
+      }
+      if (Grp::kSingle) qs_frag_load(g, s + o, q, base, xf);  // lands during the reductions and pass 2
     }
     g.sum4(dot1, zz, dd, zd);
     dot1 = wb0 * dz0 + dot1;
     const double y0 = w_head(e, wb0, dot1, dz0);
     // pass 2: w.(d - wdz)
     double dot2 = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double yt = w_tail(e, 1.0, wbar[o + t], dot1, dz[o + t]);
-      if (wdz) wdz[o + t] = yt;
-      dot2 += wbar[o + t] * (d[o + t] - yt);
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, dz + o, q, base, gf);
+        qs_frag_load(g, d + o, q, base, df);
+      }
+      QS_FRAG(r, t) {
+        const double yt = w_tail(e, 1.0, wf[r], dot1, gf[r]);
+        if (QS_TAIL_OK(t, q)) {
+          if (wdz) wdz[o + t] = yt;
+          dot2 += wf[r] * (df[r] - yt);
+        }
+      }
     }
     const double e0 = d0 - y0;
     dot2 = wb0 * e0 + g.sum(dot2);
     const double ds0 = w_head(e, wb0, dot2, e0);
     // pass 3: ds and the (s, ds) quadratic
     double ss = 0.0, d2 = 0.0, sd = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) {
-      const double yt = w_tail(e, 1.0, wbar[o + t], dot1, dz[o + t]);
-      const double dst = w_tail(e, 1.0, wbar[o + t], dot2, d[o + t] - yt);
-      ds[o + t] = dst;
-      const double st = s[o + t];
-      ss += st * st;
-      d2 += dst * dst;
-      sd += st * dst;
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, dz + o, q, base, gf);
+        qs_frag_load(g, d + o, q, base, df);
+        qs_frag_load(g, s + o, q, base, xf);
+      }
+      QS_FRAG(r, t) {
+        const double yt = w_tail(e, 1.0, wf[r], dot1, gf[r]);
+        const double dst = w_tail(e, 1.0, wf[r], dot2, df[r] - yt);
+        if (QS_TAIL_OK(t, q)) {
+          ds[o + t] = dst;
+          const double st = xf[r];
+          ss += st * st;
+          d2 += dst * dst;
+          sd += st * dst;
+        }
+      }
     }
     g.sum3(ss, d2, sd);
     if (g.lane() == 0 && q) {
       if (wdz) wdz[o] = y0;
       ds[o] = ds0;
+    }
+    // every thread holds all eight sums: lane 0 finishes the (s, ds) pair and lane 1 the (z, dz) pair side by
+    // side (each is a sqrt + divisions chain); a one-lane group does both
+    if (g.size() >= 2) {
+      if (g.lane() < 2 && q) {
+        const bool zs = g.lane() == 1;
+        const double u0 = zs ? z0 : s0, du0 = zs ? dz0 : ds0, uu = zs ? zz : ss, d_d = zs ? dd : d2, ud = zs ? zd : sd;
+        const double viol = sqrt(uu) - u0;
+        const double step = qs_soc_step(du0 * du0 - d_d, 2.0 * (u0 * du0 - ud), u0 * u0 - uu);
+        if (zs) {
+          acc.viol_z = fmax(acc.viol_z, viol);
+          acc.step_z = fmin(acc.step_z, step);
+        } else {
+          acc.viol_s = fmax(acc.viol_s, viol);
+          acc.step_s = fmin(acc.step_s, step);
+        }
+      }
+    } else if (q) {
       acc.viol_s = fmax(acc.viol_s, sqrt(ss) - s0);
       acc.viol_z = fmax(acc.viol_z, sqrt(zz) - z0);
       acc.step_s = fmin(acc.step_s, qs_soc_step(ds0 * ds0 - d2, 2.0 * (s0 * ds0 - sd), s0 * s0 - ss));
@@ -574,6 +749,7 @@ struct PostSolveOp {
 // -------------------------------------------------- W^T W v = W (W v)  (a-13)
 // Scaling block of the KKT operator, used by the refinement residual.
 struct ApplyW2Op {
+  static constexpr bool kResident = false;
   const double* w;
   const double* eta;
   const double* wbar;
@@ -588,14 +764,35 @@ struct ApplyW2Op {
   __device__ void soc(Acc&, const Grp& g, int k, int o, int q) const {
     const double wb0 = q ? wbar[o] : 0.0, u0 = q ? u[o] : 0.0, e = q ? eta[k] : 1.0;
     double dot1 = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) dot1 += wbar[o + t] * u[o + t];
+    double wf[Grp::kR], uf[Grp::kR];
+    QS_CHUNKS(base) {
+      qs_frag_load(g, wbar + o, q, base, wf);
+      qs_frag_load(g, u + o, q, base, uf);
+#pragma unroll
+      for (int r = 0; r < Grp::kR; ++r) dot1 += wf[r] * uf[r];
+    }
     dot1 = wb0 * u0 + g.sum(dot1);
     const double y0 = w_head(e, wb0, dot1, u0);
     double dot2 = 0.0;
-    for (int t = 1 + g.lane(); t < q; t += g.size()) dot2 += wbar[o + t] * w_tail(e, 1.0, wbar[o + t], dot1, u[o + t]);
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, u + o, q, base, uf);
+      }
+      QS_FRAG(r, t) {
+        if (QS_TAIL_OK(t, q)) dot2 += wf[r] * w_tail(e, 1.0, wf[r], dot1, uf[r]);
+      }
+    }
     dot2 = wb0 * y0 + g.sum(dot2);
-    for (int t = 1 + g.lane(); t < q; t += g.size())
-      out[o + t] = w_tail(e, 1.0, wbar[o + t], dot2, w_tail(e, 1.0, wbar[o + t], dot1, u[o + t]));
+    QS_CHUNKS(base) {
+      if (!Grp::kSingle) {
+        qs_frag_load(g, wbar + o, q, base, wf);
+        qs_frag_load(g, u + o, q, base, uf);
+      }
+      QS_FRAG(r, t) {
+        if (QS_TAIL_OK(t, q)) out[o + t] = w_tail(e, 1.0, wf[r], dot2, w_tail(e, 1.0, wf[r], dot1, uf[r]));
+      }
+    }
     if (g.lane() == 0 && q) out[o] = w_head(e, wb0, dot2, y0);
   }
   __device__ void finish(Acc&) const {}

@@ -126,6 +126,47 @@ void hs_kkt_assemble(const KktDims& d, const i64* Pp, const i64* Pi, const doubl
   }
 }
 
+// Column pointers of the full KKT matrix and the COMPACT pattern (the same matrix without the off-diagonal
+// entries of the dense SOC blocks) in O(N + nnz(P, A, G)).  The device fills the entries of the full matrix
+// (kkt_kernels.cu: qsk_kkt_fill); the analysis needs only the compact pattern plus the clique ranges.
+void hs_kkt_pattern(const KktDims& d, const i64* Pp, const i64* Pi, const i64* Arp, const i64* Ari, const i64* Grp,
+                    const i64* Gri, i64* Kp, std::vector<i64>* Kcp_out, std::vector<i64>* Kci_out) {
+  const i64 n = d.n, p = d.p, l = d.l, m = d.m, N = n + p + m;
+  std::vector<i64>& Kcp = *Kcp_out;
+  std::vector<i64>& Kci = *Kci_out;
+  Kcp.assign(N + 1, 0);
+  Kci.clear();
+  Kci.reserve(Pp[n] + n + Arp[p] + p + Grp[m] + m);
+  Kp[0] = 0;
+  for (i64 j = 0; j < n; ++j) {
+    for (i64 k = Pp[j]; k < Pp[j + 1]; ++k) Kci.push_back(Pi[k]);
+    if (!p_has_diag(Pp, Pi, j)) Kci.push_back(j);
+    Kcp[j + 1] = (i64)Kci.size();
+    Kp[j + 1] = Kcp[j + 1];
+  }
+  for (i64 r = 0; r < p; ++r) {
+    for (i64 k = Arp[r]; k < Arp[r + 1]; ++k) Kci.push_back(Ari[k]);
+    Kci.push_back(n + r);
+    Kcp[n + r + 1] = (i64)Kci.size();
+    Kp[n + r + 1] = Kcp[n + r + 1];
+  }
+  const i64 base = n + p;
+  i64 at = Kp[base];
+  auto conic_col = [&](i64 c, i64 block_entries) {
+    for (i64 k = Grp[c]; k < Grp[c + 1]; ++k) Kci.push_back(Gri[k]);
+    Kci.push_back(base + c);
+    Kcp[base + c + 1] = (i64)Kci.size();
+    at += (Grp[c + 1] - Grp[c]) + block_entries;
+    Kp[base + c + 1] = at;
+  };
+  for (i64 i = 0; i < l; ++i) conic_col(i, 1);
+  i64 o = l;
+  for (i64 k = 0; k < d.nsoc; ++k) {
+    for (i64 j = 0; j < d.q[k]; ++j) conic_col(o + j, j + 1);
+    o += d.q[k];
+  }
+}
+
 // ------------------------------------------------------- symmetric graph build
 namespace {
 

@@ -28,6 +28,11 @@ void hs_kkt_assemble(const KktDims& d, const i64* Pp, const i64* Pi, const doubl
                      const double* Arx, const i64* Grp, const i64* Gri, const double* Grx, i64* Kp, i64* Ki,
                      double* Kx, i64* positions, i64* slot_offsets, i64* soc_slot_starts);
 
+// Kp = column pointers of the full KKT matrix; (Kcp, Kci) = its pattern without the off-diagonal entries of the
+// dense SOC blocks (what hs_symbolic_cliques needs next to the clique ranges).  O(N + nnz(P, A, G)).
+void hs_kkt_pattern(const KktDims& d, const i64* Pp, const i64* Pi, const i64* Arp, const i64* Ari, const i64* Grp,
+                    const i64* Gri, i64* Kp, std::vector<i64>* Kcp, std::vector<i64>* Kci);
+
 // ---- symbolic analysis ------------------------------------------------------
 struct Symbolic {
   i64 N = 0;

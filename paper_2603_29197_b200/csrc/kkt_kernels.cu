@@ -136,6 +136,142 @@ __global__ void __launch_bounds__(QS_THREADS)
   }
 }
 
+
+// ------------------------------------------------------------ staged variant
+// Whole conic K columns are adjacent in K.values (a conic column is its G'
+// entries followed by its block entries, and the next column starts where it
+// ends), and so are the packed slots of adjacent SOC columns.  A tile of
+// columns therefore owns ONE contiguous run of the output.  The CTA builds that
+// run in shared memory (half-warp per column, as in the streaming kernel) and
+// hands it to the TMA engine as 16-byte-aligned bulk stores
+// (cp.async.bulk.global.shared::cta): HBM sees full, aligned lines only, the
+// SM's LSU issues no global stores, and the next CTA of the SM computes while
+// this one's stores drain.  An odd first/last element goes out as a scalar.
+//   SLOTS : run = slot range of the tile's columns
+//   DIRECT: run = [kstart[col0], kstart[col1]) with kstart = K.col_pointers + n + p
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+template <int MODE, bool BULK>
+__global__ void __launch_bounds__(QS_THREADS)
+    k_neg_wtw_staged(int l, int nb_orth, const double* __restrict__ w, const double* __restrict__ wbar,
+                     const int* __restrict__ soc_ptr, const int* __restrict__ cone_of_col,
+                     const int* __restrict__ tile_ptr, const double* __restrict__ c4, const double* __restrict__ e2,
+                     const i64* __restrict__ slot_start, const i64* __restrict__ kstart,
+                     const int* __restrict__ g_ptr, const double* __restrict__ g_val, double* __restrict__ out) {
+  if ((int)blockIdx.x < nb_orth) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l; i += nb_orth * blockDim.x) {
+      const double v = -(w[i] * w[i]);
+      if (MODE == MODE_SLOTS) out[i] = v;
+      if (MODE == MODE_DIRECT) out[kstart[i + 1] - 1] = v;
+    }
+    return;
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* buf = reinterpret_cast<double*>(smem_raw);          // [QS_WTW_STAGE + 4] the output run
+  double* mA = buf + QS_WTW_STAGE + 4;                         // per-column constants, structure of arrays
+  double* mA0 = mA + QS_WTW_SCOLS;
+  double* mne2 = mA0 + QS_WTW_SCOLS;
+  int* mj = reinterpret_cast<int*>(mne2 + QS_WTW_SCOLS);       // row count - 1 of the block part
+  int* mdst = mj + QS_WTW_SCOLS;                               // offset of the column's first entry in buf
+  int* mng = mdst + QS_WTW_SCOLS;                              // G' entries in front of the block part
+  int* mo = mng + QS_WTW_SCOLS;                                // first wbar index of the column's cone
+  int* mg0 = mo + QS_WTW_SCOLS;                                // first entry of G's CSR row
+  double* wst = reinterpret_cast<double*>(mg0 + QS_WTW_SCOLS); // [QS_WTW_SWIN] wbar window of the tile's cones
+  __shared__ i64 run[2];
+  __shared__ int win[2];
+  const int tile = blockIdx.x - nb_orth;
+  const int col0 = tile_ptr[tile], col1 = tile_ptr[tile + 1];
+  const int ncols = col1 - col0;
+  if (threadIdx.x == 0) {
+    if (MODE == MODE_DIRECT) {
+      run[0] = kstart[col0];
+      run[1] = kstart[col1];
+    } else {
+      const int ka = cone_of_col[col0 - l], kb = cone_of_col[col1 - 1 - l];
+      const i64 ja = col0 - soc_ptr[ka], jb = col1 - 1 - soc_ptr[kb];
+      run[0] = slot_start[ka] + ja * (ja + 1) / 2;
+      run[1] = slot_start[kb] + (jb + 1) * (jb + 2) / 2;
+    }
+    win[0] = soc_ptr[cone_of_col[col0 - l]];  // column c of cone k reads wbar[soc_ptr[k] .. c]: window [win0, col1)
+  }
+  __syncthreads();
+  const i64 r0 = run[0], r1 = run[1];
+  const int wlo = win[0], wlen = col1 - wlo;
+  const bool wstaged = wlen <= QS_WTW_SWIN;
+  if (wstaged)
+    for (int t = threadIdx.x; t < wlen; t += QS_THREADS) wst[t] = wbar[wlo + t];
+  const int shift = (int)(r0 & 1);  // global even indices land on even (16-byte aligned) shared indices
+  // phase 0: one thread per column gathers the column constants (all columns' load chains run in parallel)
+  for (int c = threadIdx.x; c < ncols; c += QS_THREADS) {
+    const int col = col0 + c;
+    const int k = cone_of_col[col - l];
+    const int o = soc_ptr[k];
+    const int j = col - o;
+    const double cc = c4[k], ne2 = -e2[k], wj = wbar[col];
+    mne2[c] = ne2;
+    mj[c] = j;
+    mo[c] = o;
+    mA[c] = (j == 0) ? 0.0 : ne2 * ((cc + 4.0) * wj);
+    mA0[c] = (j == 0) ? ne2 * ((cc - 4.0) * wj) : ne2 * (cc * wj);
+    if (MODE == MODE_DIRECT) {
+      const i64 cs = kstart[col];
+      mdst[c] = shift + (int)(cs - r0);
+      mng[c] = (int)(kstart[col + 1] - cs) - (j + 1);
+      mg0[c] = g_ptr[col];
+    } else {
+      mdst[c] = shift + (int)(slot_start[k] + (i64)j * (j + 1) / 2 - r0);
+      mng[c] = 0;
+    }
+  }
+  __syncthreads();
+  // phase 1: half a warp per column fills the run in shared memory
+  const int hw = threadIdx.x >> 4, sl = threadIdx.x & 15;
+  for (int c = hw; c < ncols; c += QS_THREADS / 16) {
+    const int j = mj[c];
+    const double A = mA[c], ne2 = mne2[c];
+    double* dst = buf + mdst[c];
+    if (MODE == MODE_DIRECT) {
+      const int ng = mng[c], g0 = mg0[c];
+      for (int t = sl; t < ng; t += 16) dst[t] = g_val[g0 + t];
+      dst += ng;
+    }
+    const double* wc = wstaged ? wst + (mo[c] - wlo) : wbar + mo[c];
+#pragma unroll 4
+    for (int i = sl; i <= j; i += 16) {
+      double v = A * wc[i];
+      if (i == 0) v = (j == 0) ? mA0[c] * wc[0] + ne2 : mA0[c] * wc[0];
+      else if (i == j) v = v + ne2;
+      dst[i] = v;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> visible to the bulk engine
+  __syncthreads();
+  // phase 2: the run leaves as 16-byte aligned bulk stores
+  const int total = (int)(r1 - r0);
+  const int nbulk = (total - shift) & ~1;  // doubles moved by bulk stores
+  if (!BULK) {  // comparison variant: the same run leaves as aligned 128-bit stores issued by every thread
+    const double2* src = reinterpret_cast<const double2*>(buf + 2 * shift);
+    double2* dst = reinterpret_cast<double2*>(out + r0 + shift);
+    for (int i = threadIdx.x; i < nbulk / 2; i += QS_THREADS) dst[i] = src[i];
+    if (threadIdx.x == 0) {
+      if (shift) out[r0] = buf[1];
+      if ((total - shift) & 1) out[r1 - 1] = buf[shift + total - 1];
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const i64 g0 = r0 + shift;
+    if (nbulk > 0)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + g0),
+                   "r"(smem_addr(buf + 2 * shift)), "r"(nbulk * 8)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (shift) out[r0] = buf[1];
+    if ((total - shift) & 1) out[r1 - 1] = buf[shift + total - 1];
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory must outlive the reads
+  }
+}
+
 // positions[slot] == closed form for every slot?  flag[0] set to 1 otherwise.
 __global__ void __launch_bounds__(QS_THREADS)
     k_check_direct(int l, int nb_orth, const int* soc_ptr, const int* cone_of_col, const int* tile_ptr,
@@ -158,6 +294,69 @@ __global__ void __launch_bounds__(QS_THREADS)
   if (bad) *flag = 1;
 }
 
+// KKT assembly on the device (reference: assemble_kkt, kkt.py:55-135): one warp per K column writes the row
+// indices, the initial values and the slot -> position map of that column.  Column layout (upper triangle, rows
+// ascending): x column j = P(:, j) plus an explicit diagonal; equality column = row of A then its zero diagonal;
+// conic column = row of G, then the -I block entries (orthant: the diagonal; SOC column j: rows o .. o+j).
+__global__ void __launch_bounds__(QS_THREADS)
+    k_kkt_fill(int n, int p, int m, int l, Csr Pu, Csr Ar, Csr Gr, const int* __restrict__ soc_ptr,
+               const int* __restrict__ cone_of_col, const i64* __restrict__ slot_start, const i64* __restrict__ Kp,
+               int* __restrict__ Ki, double* __restrict__ Kx, i64* __restrict__ pos) {
+  const i64 col = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (col >= (i64)n + p + m) return;
+  i64 at = Kp[col];
+  if (col < n) {
+    const int b = Pu.ptr[col], e = Pu.ptr[col + 1];
+    for (int k = b + lane; k < e; k += 32) {
+      const int i = Pu.idx[k];
+      Ki[at + (k - b)] = i;
+      Kx[at + (k - b)] = (i == col) ? Pu.val[k] + 0.0 : Pu.val[k];  // the explicit 0.0 diagonal is summed onto P_jj
+    }
+    if (lane == 0 && !(e > b && Pu.idx[e - 1] == col)) {
+      Ki[at + (e - b)] = (int)col;
+      Kx[at + (e - b)] = 0.0;
+    }
+    return;
+  }
+  if (col < n + p) {
+    const int r = (int)(col - n);
+    const int b = Ar.ptr[r], e = Ar.ptr[r + 1];
+    for (int k = b + lane; k < e; k += 32) {
+      Ki[at + (k - b)] = Ar.idx[k];
+      Kx[at + (k - b)] = Ar.val[k];
+    }
+    if (lane == 0) {
+      Ki[at + (e - b)] = (int)col;
+      Kx[at + (e - b)] = 0.0;
+    }
+    return;
+  }
+  const int c = (int)(col - n - p);
+  const int b = Gr.ptr[c], e = Gr.ptr[c + 1];
+  for (int k = b + lane; k < e; k += 32) {
+    Ki[at + (k - b)] = Gr.idx[k];
+    Kx[at + (k - b)] = Gr.val[k];
+  }
+  at += e - b;
+  if (c < l) {
+    if (lane == 0) {
+      Ki[at] = (int)col;
+      Kx[at] = -1.0;
+      pos[c] = at;
+    }
+    return;
+  }
+  const int k = cone_of_col[c - l];
+  const int o = soc_ptr[k], j = c - o;
+  const i64 sb = slot_start[k] + (i64)j * (j + 1) / 2;
+  for (int i = lane; i <= j; i += 32) {
+    Ki[at + i] = n + p + o + i;
+    Kx[at + i] = (i == j) ? -1.0 : 0.0;
+    pos[sb + i] = at + i;
+  }
+}
+
 int orth_blocks(int l) {
   if (l <= 0) return 0;
   int nb = (l + QS_THREADS - 1) / QS_THREADS;
@@ -174,6 +373,33 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
   const int nb_orth = orth_blocks(P.l);
   const int grid = nb_orth + P.ntiles;
   if (grid == 0) return;
+  // Staged bulk-store path (opt-in, QS_WTW_STAGED=1): contiguous output run per tile (dense slots, or whole K
+  // columns), 16-byte aligned base.  Measured on B200 at C4 it is SLOWER than the streaming kernel below (360 us
+  // vs 212 us: three dependent phases per tile with CTA-wide barriers and only 4 CTAs per SM leave the SM waiting
+  // on latency), so the streaming kernel stays the default; see DESIGN.md section 3.
+  if ((mode == MODE_SLOTS || (mode == MODE_DIRECT && P.g_ptr && P.kstart)) && P.stile_ptr &&
+      (reinterpret_cast<uintptr_t>(out) & 15) == 0 && getenv("QS_WTW_STAGED")) {
+    const bool direct = mode == MODE_DIRECT;
+    const int nt = direct ? P.n_stiles_direct : P.n_stiles_slots;
+    const int* tp = direct ? P.stile_ptr_direct : P.stile_ptr;
+    const size_t sm = (size_t)(QS_WTW_STAGE + 4 + QS_WTW_SWIN) * sizeof(double) +
+                      (size_t)QS_WTW_SCOLS * (3 * sizeof(double) + 5 * sizeof(int));
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<nb_orth + nt, QS_THREADS, sm, st>>>(P.l, nb_orth, w, wbar, P.soc_ptr, P.cone_of_col, tp, P.c4, P.e2,
+                                                 P.slot_start, P.kstart, P.g_ptr, P.g_val, out);
+    };
+    if (nb_orth + nt == 0) return;
+    const bool bulk = !getenv("QS_WTW_PLAIN");
+    if (direct) {
+      if (bulk) go(k_neg_wtw_staged<MODE_DIRECT, true>);
+      else go(k_neg_wtw_staged<MODE_DIRECT, false>);
+    } else {
+      if (bulk) go(k_neg_wtw_staged<MODE_SLOTS, true>);
+      else go(k_neg_wtw_staged<MODE_SLOTS, false>);
+    }
+    return;
+  }
   const bool staged = P.max_tile_window <= QS_WTW_WCAP;
   const int wcap = staged ? P.max_tile_window : 0;
   const int mc = P.max_tile_cols;
@@ -193,6 +419,14 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
     if (staged) launch(k_neg_wtw<MODE_DIRECT, true>, nullptr, P.kp_conic);
     else launch(k_neg_wtw<MODE_DIRECT, false>, nullptr, P.kp_conic);
   }
+}
+
+void qsk_kkt_fill(const WtwPlan& P, int n, int p, const Csr& Pu, const Csr& Ar, const Csr& Gr, const i64* Kp, int* Ki,
+                  double* Kx, i64* pos, cudaStream_t st) {
+  const i64 N = (i64)n + p + P.m;
+  const i64 blocks = (N * 32 + QS_THREADS - 1) / QS_THREADS;
+  k_kkt_fill<<<(unsigned)blocks, QS_THREADS, 0, st>>>(n, p, P.m, P.l, Pu, Ar, Gr, P.soc_ptr, P.cone_of_col,
+                                                      P.slot_start, Kp, Ki, Kx, pos);
 }
 
 void qsk_check_direct_map(const WtwPlan& P, const i64* positions, int* flag, cudaStream_t st) {

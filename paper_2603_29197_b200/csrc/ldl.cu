@@ -124,6 +124,55 @@ __global__ void __launch_bounds__(LDL_THREADS)
   }
 }
 
+// List-driven extend-add (see AsmLists): a warp owns (column slot, row band) of a front outright and walks the
+// slot's child entries in their fixed order -- deterministic, no atomics, no searching.
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_extend_add_list(DevSym S, AsmLists A, const EaItem* items, i64 nitems, double* L, double* U) {
+  const i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nitems) return;
+  const EaItem it = items[w];
+  const int s = A.slot_front[it.slot], pc = A.slot_row[it.slot];
+  const Front f = front_of(S, s, L, U);
+  const i64 nr = f.nr, nu = f.nu;
+  double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;  // indexed by parent row
+  const i64 e0 = A.gptr[it.slot], e1 = A.gptr[it.slot + 1];
+  for (i64 e = e0; e < e1; ++e) {
+    const int c = A.gchild[e];
+    const int cc = A.gsrc[e] - (int)S.Boff[c];
+    const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - (S.col0[c + 1] - S.col0[c]);
+    int r_lo = cc, r_hi = nuc;
+    if (it.band >= 0) {
+      const int* bs = A.bandstart + A.bandptr[c];
+      r_lo = max(cc, bs[it.band]);
+      r_hi = bs[it.band + 1];
+    }
+    const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+    const int* rel = S.rel + S.relptr[c];
+    for (int r = r_lo + lane; r < r_hi; r += 32) dstcol[rel[r]] += Ucol[r];
+  }
+}
+
+// List-driven forward-solve gather: `tpr` lanes per slot sum the slot's child contributions in a fixed order.
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_gather_fwd_list(AsmLists A, i64 slot0, i64 nslots, int tpr, double* xw, double* B) {
+  const i64 g = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / tpr;
+  const int lane = threadIdx.x & (tpr - 1);
+  const unsigned mask = tpr == 32 ? 0xffffffffu : (((1u << tpr) - 1u) << (threadIdx.x & 31 & ~(tpr - 1)));
+  double acc = 0.0;
+  const bool on = g < nslots;
+  if (on) {
+    const i64 e1 = A.gptr[slot0 + g + 1];
+    for (i64 e = A.gptr[slot0 + g] + lane; e < e1; e += tpr) acc += B[A.gsrc[e]];
+  }
+  for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
+  if (on && lane == 0) {
+    const i64 d = A.gdst[slot0 + g];
+    if (d >= 0) xw[d] += acc;
+    else B[-d - 1] = acc;
+  }
+}
+
 // Leaf fronts with one pivot column and at most 33 rows (the private x columns
 // of a cone block: millions of them): one warp per front.
 __global__ void __launch_bounds__(LDL_THREADS)
@@ -624,12 +673,12 @@ T* upload(const std::vector<T>& v, std::vector<void*>* owned, size_t* bytes, cud
 
 }  // namespace
 
-std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, const i64* d_Kp, const int* d_Ki, int order,
+std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full, const i64* d_Kp, const int* d_Ki, int order,
                             const i64* user_perm, i64 ncliques, const i64* clique_start, const i64* clique_size,
                             i64 n_pos, double static_reg, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
   N = N_;
-  knnz = Kp[N];
+  knnz = knnz_full;
   std::string err = hs_symbolic_cliques(N, Kp, Ki, order, user_perm, ncliques, clique_start, clique_size, &S);
   if (!err.empty()) return err;
   D.nsup = S.nsup;
@@ -713,6 +762,121 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, const i64* d_K
   device_bytes += pmax * 8;
   d_slabs = upload(slabs, &owned, &device_bytes, st);
   if (!d_leaf || !d_gen || !d_small || !d_blk || !d_slabs) return "cudaMalloc failed for LDL work lists";
+  // ---- assembly lists (AsmLists): slots of the fronts that have children, level by level
+  use_lists = getenv("QS_LDL_SEARCH") == nullptr && S.Boff[S.nsup] < ((i64)1 << 31);
+  if (use_lists) {
+    std::vector<i64> slot_base(S.nsup, -1);
+    std::vector<int> slot_front, slot_row;
+    lvslot.assign(S.nlevels + 1, 0);
+    for (int lv = 0; lv < S.nlevels; ++lv) {
+      for (int k = S.levelptr[lv]; k < S.levelptr[lv + 1]; ++k) {
+        const int s = S.levelsup[k];
+        if (S.childptr[s + 1] == S.childptr[s]) continue;
+        const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
+        slot_base[s] = (i64)slot_front.size();
+        for (int r = 0; r < nr; ++r) {
+          slot_front.push_back(s);
+          slot_row.push_back(r);
+        }
+      }
+      lvslot[lv + 1] = (i64)slot_front.size();
+    }
+    const i64 nslots = (i64)slot_front.size();
+    std::vector<i64> gptr(nslots + 1, 0), gdst(nslots);
+    for (int c = 0; c < S.nsup; ++c) {
+      const int par = S.parent[c];
+      if (par < 0) continue;
+      for (i64 t = S.relptr[c]; t < S.relptr[c + 1]; ++t) gptr[slot_base[par] + S.rel[t] + 1]++;
+    }
+    for (i64 k = 0; k < nslots; ++k) gptr[k + 1] += gptr[k];
+    std::vector<int> gsrc(gptr[nslots]), gchild(gptr[nslots]);
+    {
+      std::vector<i64> next(gptr.begin(), gptr.end() - 1);
+      for (int s = 0; s < S.nsup; ++s)  // children in their fixed (ascending) order
+        for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci) {
+          const int c = S.child[ci];
+          const i64 nuc = S.relptr[c + 1] - S.relptr[c];
+          for (i64 t = 0; t < nuc; ++t) {
+            const i64 e = next[slot_base[s] + S.rel[S.relptr[c] + t]]++;
+            gsrc[e] = (int)(S.Boff[c] + t);
+            gchild[e] = c;
+          }
+        }
+    }
+    for (i64 k = 0; k < nslots; ++k) {
+      const int s = slot_front[k], r = slot_row[k];
+      const int ns = S.col0[s + 1] - S.col0[s];
+      gdst[k] = (r < ns) ? (i64)(S.col0[s] + r) : -(S.Boff[s] + (r - ns)) - 1;
+    }
+    // row bands for fronts with many children
+    std::vector<i64> bandptr(S.nsup + 1, 0);
+    std::vector<char> banded(S.nsup, 0);
+    for (int s = 0; s < S.nsup; ++s) {
+      const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
+      banded[s] = (S.childptr[s + 1] - S.childptr[s] >= 64 && nr > QS_EA_BAND);
+    }
+    for (int c = 0; c < S.nsup; ++c) {
+      const int par = S.parent[c];
+      i64 cntb = 0;
+      if (par >= 0 && banded[par]) {
+        const int nrp = (int)(S.rowptr[par + 1] - S.rowptr[par]);
+        cntb = (nrp + QS_EA_BAND - 1) / QS_EA_BAND + 1;
+      }
+      bandptr[c + 1] = bandptr[c] + cntb;
+    }
+    std::vector<int> bandstart(std::max<i64>(bandptr[S.nsup], 1));
+    for (int c = 0; c < S.nsup; ++c) {
+      const i64 nb1 = bandptr[c + 1] - bandptr[c];
+      if (!nb1) continue;
+      const int* rel = S.rel.data() + S.relptr[c];
+      const int nuc = (int)(S.relptr[c + 1] - S.relptr[c]);
+      int r = 0;
+      for (i64 b = 0; b < nb1; ++b) {
+        while (r < nuc && rel[r] < b * QS_EA_BAND) ++r;
+        bandstart[bandptr[c] + b] = r;
+      }
+    }
+    // extend-add items per level
+    std::vector<EaItem> items;
+    eaptr.assign(S.nlevels + 1, 0);
+    lv_tpr.assign(S.nlevels, 1);
+    for (int lv = 0; lv < S.nlevels; ++lv) {
+      for (i64 k = lvslot[lv]; k < lvslot[lv + 1]; ++k) {
+        if (gptr[k + 1] == gptr[k]) continue;  // nothing lands on this column
+        const int s = slot_front[k];
+        if (!banded[s]) {
+          items.push_back(EaItem{(int)k, -1});
+        } else {
+          const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
+          const int nbands = (nr + QS_EA_BAND - 1) / QS_EA_BAND;
+          for (int b = slot_row[k] / QS_EA_BAND; b < nbands; ++b) items.push_back(EaItem{(int)k, b});
+        }
+      }
+      eaptr[lv + 1] = (i64)items.size();
+      const i64 ns_lv = lvslot[lv + 1] - lvslot[lv];
+      const double mean = ns_lv ? (double)(gptr[lvslot[lv + 1]] - gptr[lvslot[lv]]) / (double)ns_lv : 1.0;
+      int t = 1;
+      while (t < 32 && t * 2 <= mean) t <<= 1;
+      lv_tpr[lv] = t;
+    }
+    if (nslots >= ((i64)1 << 31)) {
+      use_lists = false;
+    } else {
+      A.gptr = upload(gptr, &owned, &device_bytes, st);
+      A.gsrc = upload(gsrc, &owned, &device_bytes, st);
+      A.gchild = upload(gchild, &owned, &device_bytes, st);
+      A.gdst = upload(gdst, &owned, &device_bytes, st);
+      A.slot_front = upload(slot_front, &owned, &device_bytes, st);
+      A.slot_row = upload(slot_row, &owned, &device_bytes, st);
+      A.bandptr = upload(bandptr, &owned, &device_bytes, st);
+      A.bandstart = upload(bandstart, &owned, &device_bytes, st);
+      d_eaitems = upload(items, &owned, &device_bytes, st);
+      if (!A.gptr || !A.gsrc || !A.gchild || !A.gdst || !A.slot_front || !A.slot_row || !A.bandptr || !A.bandstart ||
+          !d_eaitems)
+        return "cudaMalloc failed for the LDL assembly lists";
+      cudaStreamSynchronize(st);  // the host vectors above die at the end of this block
+    }
+  }
   std::vector<double> regh(N);
   for (i64 k = 0; k < N; ++k) regh[k] = (S.perm[k] < n_pos) ? static_reg : -static_reg;  // kkt.py:48-52
   reg = upload(regh, &owned, &device_bytes, st);
@@ -748,7 +912,14 @@ void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
         D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars);
   for (int lv = 0; lv < S.nlevels; ++lv) {
     const int nslab = slabptr[lv + 1] - slabptr[lv];
-    if (nslab > 0) k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
+    if (use_lists) {
+      const i64 ni = eaptr[lv + 1] - eaptr[lv];
+      if (ni > 0)
+        k_extend_add_list<<<(unsigned)((ni * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+            D, A, d_eaitems + eaptr[lv], ni, L, U);
+    } else if (nslab > 0) {
+      k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
+    }
     const int cnt = smallptr[lv + 1] - smallptr[lv];
     if (cnt > 0)
       k_front_factor<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, U, Dg, reg, dyn_eps, scalars);
@@ -787,7 +958,14 @@ void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
   if (n_leaf > 0) k_leaf_fwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw, B);
   for (int lv = 0; lv < S.nlevels; ++lv) {
     const int nslab = slabptr[lv + 1] - slabptr[lv];
-    if (nslab > 0) k_gather_fwd<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], xw, B);
+    if (use_lists) {
+      const i64 nsl = lvslot[lv + 1] - lvslot[lv];
+      if (nsl > 0)
+        k_gather_fwd_list<<<(unsigned)((nsl * lv_tpr[lv] + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+            A, lvslot[lv], nsl, lv_tpr[lv], xw, B);
+    } else if (nslab > 0) {
+      k_gather_fwd<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], xw, B);
+    }
     const int cnt = smallptr[lv + 1] - smallptr[lv];
     if (cnt > 0) k_solve_fwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw, B);
     for (int b0 = blkptr[lv]; b0 < blkptr[lv + 1]; b0 += 65535) {

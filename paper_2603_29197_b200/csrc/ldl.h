@@ -41,6 +41,32 @@ struct SlabItem {
   int front, c_lo;
 };
 
+// Assembly lists built at analysis.  A "slot" is one (front, local row) pair of a front that has children; the
+// slots of a level are contiguous.  Slot lists hold, in child order, every child entry that lands on that row:
+//   gptr[slot] .. gptr[slot+1]   range in gsrc / gchild
+//   gsrc[e]    offset of the entry in the solve contribution storage B (= Boff[child] + position in the child)
+//   gchild[e]  the child supernode
+//   gdst[slot] where the forward-solve sum goes: >= 0 -> xw[gdst] += sum,  < 0 -> B[-gdst-1] = sum
+// By symmetry the same list serves the numeric extend-add: entry e of column slot (s, pc) is child column
+// cc = gsrc[e] - Boff[child], whose rows cc.. are added into column pc of the front.
+// Fronts with many children are cut into row bands of QS_EA_BAND rows so that several warps share one column:
+// bandptr[child] .. : for each band b of the PARENT, the first child update row whose parent row is >= b * BAND.
+#define QS_EA_BAND 256
+struct AsmLists {
+  const i64* gptr;
+  const int* gsrc;
+  const int* gchild;
+  const i64* gdst;
+  const int* slot_front;  // [nslots]
+  const int* slot_row;    // [nslots] local row / column of the slot inside its front
+  const i64* bandptr;     // [nsup+1] offsets into bandstart (only children of banded fronts have entries)
+  const int* bandstart;
+};
+// extend-add work item of the list-driven kernel: column slot + row band (band = -1: whole column)
+struct EaItem {
+  int slot, band;
+};
+
 struct LinSys {
   Symbolic S;
   DevSym D{};
@@ -64,13 +90,19 @@ struct LinSys {
   i64* d_poff = nullptr;   // per blocked front: offset into `partial`
   double* partial = nullptr;  // backward-solve row-tile partial sums
   std::vector<int> genptr, slabptr, smallptr, blkptr, blk_max_ns, blk_max_nr, blk_max_nu;
+  AsmLists A{};
+  EaItem* d_eaitems = nullptr;
+  std::vector<i64> lvslot, eaptr;   // per level: slot range, extend-add item range
+  std::vector<int> lv_tpr;          // per level: lanes per slot in the forward-solve gather
+  bool use_lists = true;
   std::vector<void*> owned;
   double dyn_eps = 1e-14;
   double analysis_seconds = 0.0;
   size_t device_bytes = 0;
 
-  // Kp/Ki: host pattern (upper CSC); d_Kp/d_Ki: the same on the device.
-  std::string analyze(i64 N, const i64* Kp, const i64* Ki, const i64* d_Kp, const int* d_Ki, int order,
+  // Kp/Ki: host pattern (upper CSC) -- the full matrix or its compact form without the off-diagonal entries of
+  // the clique blocks; knnz_full / d_Kp / d_Ki: the full matrix on the device.
+  std::string analyze(i64 N, const i64* Kp, const i64* Ki, i64 knnz_full, const i64* d_Kp, const int* d_Ki, int order,
                       const i64* user_perm, i64 ncliques, const i64* clique_start, const i64* clique_size, i64 n_pos,
                       double static_reg, cudaStream_t st);
   void factor(const double* d_Kx, double* scalars, cudaStream_t st);

@@ -175,9 +175,12 @@ class DeviceSolver:
                 "direct_map")
         return dict(zip(keys, t.tolist()))
 
-    def time_kernel(self, kernel_id: int, reps: int = 20) -> float:
+    def time_kernel(self, kernel_id: int, reps: int = 20, cold: bool = False) -> float:
+        """Mean milliseconds per launch of one hot-path kernel (CUDA events on the handle's stream).  cold=True
+        flushes the L2 before every timed launch (the figure the kernel sees inside a solve)."""
         ms = C.c_double()
-        self._check(self.lib.qs_time_kernel(self.h, kernel_id, reps, C.byref(ms)))
+        fn = self.lib.qs_time_kernel_cold if cold else self.lib.qs_time_kernel
+        self._check(fn(self.h, kernel_id, reps, C.byref(ms)))
         return ms.value
 
     # -- the loop

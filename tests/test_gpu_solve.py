@@ -145,3 +145,66 @@ def test_deterministic_trace():
     for k in "xyzs":
         assert np.array_equal(getattr(a, k), getattr(b, k))
     assert a.objective == b.objective and a.iterations == b.iterations
+
+
+@pytest.mark.parametrize("name", ["portfolio_4", "group_lasso_3", "tv_denoising_8", "random_3", "soc_slice",
+                                  "cfg:group_lasso", "cfg:portfolio"])
+@pytest.mark.parametrize("staged", [False, True])
+def test_in_solver_scaling_update_matches_oracle(oracle, name, staged, monkeypatch):
+    """The resident path's KKT update (whole-column staged bulk stores, kkt_kernels.cu) leaves exactly the
+    reference's write_scaling result in K.values (kkt.py:146-150) and touches nothing else."""
+    if name == "cfg:group_lasso":  # ~45 output tiles of mixed parity, cones of 20..250
+        from paper_2603_29197_b200 import configs
+
+        d = configs.group_lasso(groups=40, qlo=20, qhi=250, samples=200, nnz_per_col=3, seed=3)
+    elif name == "cfg:portfolio":  # orthant block + SOCs, G rows of different lengths
+        from paper_2603_29197_b200 import configs
+
+        d = configs.portfolio(assets=600, factors=20, sector=50, seed=1)
+    else:
+        d = problem_from_golden(load_golden(name))
+    if staged:
+        monkeypatch.setenv("QS_WTW_STAGED", "1")  # shared-memory staging + TMA bulk stores instead of streaming
+    dev = DeviceSolver(d, Settings())
+    dev.initialize_iterate()
+    dev.compute_residuals()
+    dev.ipm_step()  # NT scaling of the initial iterate -> K.values
+    sc = dev.scaling()
+    got = dev.kkt()
+    ref = oracle.assemble_kkt(d)
+    oracle.write_scaling(ref, oracle.Scaling(d.cone, sc.w_orthant, sc.soc_eta, sc.soc_wbar, sc.lam))
+    assert np.array_equal(got.matrix.col_pointers, ref.matrix.col_pointers)
+    assert np.array_equal(got.matrix.row_indices, ref.matrix.row_indices)
+    assert np.allclose(got.matrix.values, ref.matrix.values, rtol=1e-12, atol=0)
+    mask = np.ones(got.matrix.values.size, bool)
+    mask[got.nt_entry_positions] = False
+    assert np.array_equal(got.matrix.values[mask], ref.matrix.values[mask])  # P, A', G' entries bit-identical
+    dev.close()
+
+
+@pytest.mark.parametrize("name", golden_problem_names() + ["cfg:group_lasso", "cfg:portfolio", "cfg:mpc"])
+def test_device_assembled_kkt_is_bit_exact(name, monkeypatch):
+    """KKT assembly on the device (qsk_kkt_fill) reproduces assemble_kkt (kkt.py:55-135) bit for bit: column
+    pointers, row indices, initial values and the slot -> position map; so does the host-assembly alternative."""
+    from paper_2603_29197_b200 import configs
+
+    if name == "cfg:group_lasso":
+        d = configs.group_lasso(groups=40, qlo=20, qhi=250, samples=200, nnz_per_col=3, seed=3)
+    elif name == "cfg:portfolio":
+        d = configs.portfolio(assets=600, factors=20, sector=50, seed=1)
+    elif name == "cfg:mpc":
+        d = configs.mpc(horizon=10, nx=6, nu=2, seed=2)
+    else:
+        d = problem_from_golden(load_golden(name))
+    ref = assemble_kkt(d)  # host C++ assembly, itself pinned bitwise to the reference (tests/test_host.py)
+    for host in (False, True):
+        if host:
+            monkeypatch.setenv("QS_HOST_ASSEMBLY", "1")
+        dev = DeviceSolver(d, Settings())
+        got = dev.kkt()
+        assert np.array_equal(got.matrix.col_pointers, ref.matrix.col_pointers)
+        assert np.array_equal(got.matrix.row_indices, ref.matrix.row_indices)
+        assert np.array_equal(got.matrix.values, ref.matrix.values)
+        assert np.array_equal(np.signbit(got.matrix.values), np.signbit(ref.matrix.values))
+        assert np.array_equal(got.nt_entry_positions, ref.nt_entry_positions)
+        dev.close()

@@ -109,6 +109,33 @@ def test_symbolic_analysis_is_valid_and_counts_match_oracle(oracle, name, monkey
             assert 1 <= st["nsup"] <= N and st["max_nr"] <= N
 
 
+@pytest.mark.parametrize("name", ["portfolio_4", "group_lasso_3", "tv_denoising_8", "soc_slice", "random_3"])
+def test_compact_pattern_gives_the_same_analysis(name):
+    """qs_setup hands the analysis the KKT pattern WITHOUT the off-diagonal entries of the dense SOC blocks (they
+    are implied by the clique ranges; the device writes them, host_setup.cpp: hs_kkt_pattern).  Ordering, supernodes
+    and fill must not depend on whether those entries are spelled out."""
+    d = problem_from_golden(load_golden(name))
+    kkt = assemble_kkt(d)
+    K = kkt.matrix
+    base = kkt.n + kkt.p + d.cone.orthant_dim
+    block_of = np.full(K.cols, -1, np.int64)
+    o = base
+    for k, q in enumerate(d.cone.soc_dims):
+        block_of[o:o + q] = k
+        o += q
+    cols = np.repeat(np.arange(K.cols), np.diff(K.col_pointers))
+    rows = K.row_indices
+    keep = ~((block_of[rows] >= 0) & (block_of[rows] == block_of[cols]) & (rows != cols))
+    cp = np.concatenate([[0], np.cumsum(np.bincount(cols[keep], minlength=K.cols))]).astype(np.int64)
+    compact = SimpleNamespace(matrix=SimpleNamespace(cols=K.cols, col_pointers=cp,
+                                                     row_indices=np.ascontiguousarray(rows[keep])),
+                              n=kkt.n, p=kkt.p, m=kkt.m)
+    for ordering in (0, 1):
+        pa, sa = _symbolic(kkt, ordering, d.cone)
+        pb, sb = _symbolic(compact, ordering, d.cone)
+        assert np.array_equal(pa, pb) and sa == sb, ordering
+
+
 def test_relaxed_amalgamation_pads_but_never_loses_entries(monkeypatch):
     d = problem_from_golden(load_golden("group_lasso_3"))
     kkt = assemble_kkt(d)
