@@ -790,7 +790,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
             make_csr(h, &h->Gr, m, n, Grp.data(), Gri.data(), Grx.data());
   if (!ok) return fail(h, QS_E_MEMORY, "out of device memory for the problem matrices");
   // one lane-group width for the whole dual range (three products per row)
-  h->Pf.tpr = qsk_pick_tpr(std::max(std::max(nnzP * 2, nnzA), nnzG), n);
+  h->Pf.tpr = std::min(32, qsk_pick_tpr(std::max(std::max(nnzP * 2, nnzA), nnzG), n));  // no CTA-per-row mode here
   h->At.tpr = h->Gt.tpr = h->Pf.tpr;
   h->c = h->prob_pool.upload(c, n, st);
   h->b = h->prob_pool.upload(b, p, st);

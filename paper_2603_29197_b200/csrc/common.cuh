@@ -12,6 +12,9 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+#include <utility>
+
 typedef long long i64;
 
 #define QS_THREADS 256
@@ -204,40 +207,66 @@ __device__ __forceinline__ void qs_frag_load(const Grp& g, const double* __restr
 // whole grid with the "last block finishes" pattern: each block publishes its
 // partials, takes a ticket, and the block drawing the last ticket combines all
 // partials in block order and runs `fin(result)` on thread 0.
-enum { RED_SUM = 0, RED_MIN = 1, RED_MAX = 2 };
+// RED_AMAX: max of NON-NEGATIVE doubles (|x| norms).  Their bit patterns order like unsigned integers and a
+// NaN (sign cleared by fabs) is the largest pattern, so it propagates; a warp reduces one with two REDUX
+// instructions instead of five shuffle rounds.
+enum { RED_SUM = 0, RED_MIN = 1, RED_MAX = 2, RED_AMAX = 3 };
 
 struct GridRed {
   double* partial;    // [>= gridDim.x * K]
   unsigned* counter;  // zero before the launch; left zero afterwards
 };
 
-__device__ __forceinline__ double qs_combine(double a, double b, int op) {
+// The reduction operators of a launch are COMPILE-TIME constants (RedOps<RED_MIN, RED_MAX, ...>): after
+// unrolling, every combine is a fixed two-or-three instruction sequence.  (With run-time operator codes the
+// epilogue of the residual kernel was ~1000 instructions per thread -- more than its SpMV work.)
+template <int OP>
+__device__ __forceinline__ double qs_combine(double a, double b) {
   // NaN-propagating max/min so that non-finite data is never masked
-  if (op == RED_SUM) return a + b;
-  if (a != a) return a;
-  if (b != b) return b;
-  if (op == RED_MIN) return b < a ? b : a;
-  return b > a ? b : a;
+  if (OP == RED_SUM) return a + b;
+  if (OP == RED_AMAX)
+    return ((unsigned long long)__double_as_longlong(b) > (unsigned long long)__double_as_longlong(a)) ? b : a;
+  if (OP == RED_MIN) return (a != a) ? a : ((b < a || b != b) ? b : a);
+  return (a != a) ? a : ((b > a || b != b) ? b : a);
 }
 
-__device__ __forceinline__ double qs_identity(int op) {
-  return op == RED_SUM ? 0.0 : (op == RED_MIN ? INFINITY : -INFINITY);
+template <int OP>
+__device__ __forceinline__ double qs_identity() {
+  return (OP == RED_SUM || OP == RED_AMAX) ? 0.0 : (OP == RED_MIN ? INFINITY : -INFINITY);
 }
 
-template <int K>
+template <int... OPS>
 struct RedOps {
-  int op[K];
+  static constexpr int K = sizeof...(OPS);
 };
 
-template <int K>
-__device__ __forceinline__ void qs_block_reduce(double (&v)[K], const RedOps<K>& ops, double* sm /*[32*K]*/) {
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
+// apply f.template operator()<k, OP_k>() for every k (C++17 fold over an index pack)
+template <int... OPS, class F, int... IS>
+__device__ __forceinline__ void qs_for_ops_impl(RedOps<OPS...>, F&& f, std::integer_sequence<int, IS...>) {
+  (f(std::integral_constant<int, IS>{}, std::integral_constant<int, OPS>{}), ...);
+}
+template <int... OPS, class F>
+__device__ __forceinline__ void qs_for_ops(RedOps<OPS...> o, F&& f) {
+  qs_for_ops_impl(o, static_cast<F&&>(f), std::make_integer_sequence<int, sizeof...(OPS)>{});
+}
+
+template <class Ops>
+__device__ __forceinline__ void qs_block_reduce(double (&v)[Ops::K], double* sm /*[32*K]*/) {
+  constexpr int K = Ops::K;
+  qs_for_ops(Ops{}, [&](auto kc, auto opc) {
+    constexpr int k = decltype(kc)::value, OP = decltype(opc)::value;
     double x = v[k];
+    if (OP == RED_AMAX) {
+      const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      x = __hiloint2double((int)mhi, (int)mlo);
+    } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x = qs_combine(x, __shfl_xor_sync(0xffffffffu, x, o), ops.op[k]);
+      for (int o = 16; o > 0; o >>= 1) x = qs_combine<OP>(x, __shfl_xor_sync(0xffffffffu, x, o));
+    }
     v[k] = x;
-  }
+  });
   const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) {
@@ -246,22 +275,23 @@ __device__ __forceinline__ void qs_block_reduce(double (&v)[K], const RedOps<K>&
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
+    qs_for_ops(Ops{}, [&](auto kc, auto opc) {
+      constexpr int k = decltype(kc)::value, OP = decltype(opc)::value;
       double x = sm[k];
-      for (int j = 1; j < nw; ++j) x = qs_combine(x, sm[j * K + k], ops.op[k]);
+      for (int j = 1; j < nw; ++j) x = qs_combine<OP>(x, sm[j * K + k]);
       v[k] = x;
-    }
+    });
   }
 }
 
 // After the call, thread 0 of exactly one block (the last to arrive) has run
 // fin(totals).  Every thread of every block must call this.
-template <int K, class Fin>
-__device__ __forceinline__ void qs_grid_reduce(double (&v)[K], const RedOps<K>& ops, GridRed gr, Fin fin) {
+template <class Ops, class Fin>
+__device__ __forceinline__ void qs_grid_reduce(double (&v)[Ops::K], GridRed gr, Fin fin) {
+  constexpr int K = Ops::K;
   __shared__ double sm[32 * K];
   __shared__ int last;
-  qs_block_reduce<K>(v, ops, sm);
+  qs_block_reduce<Ops>(v, sm);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) gr.partial[(size_t)blockIdx.x * K + k] = v[k];
@@ -273,14 +303,14 @@ __device__ __forceinline__ void qs_grid_reduce(double (&v)[K], const RedOps<K>& 
   if (!last) return;
   __threadfence();
   double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = qs_identity(ops.op[k]);
+  qs_for_ops(Ops{}, [&](auto kc, auto opc) { acc[decltype(kc)::value] = qs_identity<decltype(opc)::value>(); });
   for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      acc[k] = qs_combine(acc[k], __ldcg(&gr.partial[(size_t)b * K + k]), ops.op[k]);
+    qs_for_ops(Ops{}, [&](auto kc, auto opc) {
+      constexpr int k = decltype(kc)::value;
+      acc[k] = qs_combine<decltype(opc)::value>(acc[k], __ldcg(&gr.partial[(size_t)b * K + k]));
+    });
   }
-  qs_block_reduce<K>(acc, ops, sm);
+  qs_block_reduce<Ops>(acc, sm);
   if (threadIdx.x == 0) fin(acc);
 }
 

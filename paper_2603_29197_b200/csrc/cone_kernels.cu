@@ -397,10 +397,10 @@ struct MaxStepOp {
   }
   __device__ void finish(Acc& a) const {
     double v[2] = {a.step, a.viol};
-    const RedOps<2> ops = {{RED_MIN, RED_MAX}};
+    using Ops = RedOps<RED_MIN, RED_MAX>;
     double* sc = scalars;
     const int ss = slot_step, sv = slot_viol;
-    qs_grid_reduce<2>(v, ops, gr, [=](double (&t)[2]) {
+    qs_grid_reduce<Ops>(v, gr, [=](double (&t)[2]) {
       if (ss >= 0) sc[ss] = t[0];
       if (sv >= 0) sc[sv] = t[1];
     });
@@ -725,11 +725,11 @@ struct PostSolveOp {
   }
   __device__ void finish(Acc& a) const {
     double v[4] = {a.step_s, a.step_z, a.viol_s, a.viol_z};
-    const RedOps<4> ops = {{RED_MIN, RED_MIN, RED_MAX, RED_MAX}};
+    using Ops = RedOps<RED_MIN, RED_MIN, RED_MAX, RED_MAX>;
     double* sc = scalars;
     const int corr = corrector;
     const double sf = step_fraction;
-    qs_grid_reduce<4>(v, ops, gr, [=](double (&t)[4]) {
+    qs_grid_reduce<Ops>(v, gr, [=](double (&t)[4]) {
       sc[SC_STEP_S] = t[0];
       sc[SC_STEP_Z] = t[1];
       sc[SC_VIOL_S] = t[2];
@@ -810,8 +810,8 @@ __global__ void __launch_bounds__(QS_THREADS) k_mu_aff(int m, const double* s, c
     v[0] += (si + a * ds[i]) * (zi + a * dz[i]);
     v[1] += si * zi;
   }
-  const RedOps<2> ops = {{RED_SUM, RED_SUM}};
-  qs_grid_reduce<2>(v, ops, gr, [=](double (&t)[2]) {
+  using Ops = RedOps<RED_SUM, RED_SUM>;
+  qs_grid_reduce<Ops>(v, gr, [=](double (&t)[2]) {
     const double mu_aff = fmax(0.0, t[0] / deg);
     const double mu = t[1] / deg;
     double sigma = 0.0;
@@ -850,8 +850,8 @@ __global__ void __launch_bounds__(QS_THREADS) k_update_iterate(int n, int p, int
     v[0] += st * zt;
     if (!qs_finite(zt) || !qs_finite(st)) v[1] = 1.0;
   }
-  const RedOps<2> ops = {{RED_SUM, RED_MAX}};
-  qs_grid_reduce<2>(v, ops, gr, [=](double (&t)[2]) {
+  using Ops = RedOps<RED_SUM, RED_MAX>;
+  qs_grid_reduce<Ops>(v, gr, [=](double (&t)[2]) {
     scalars[SC_MU] = t[0] / deg;
     if (t[1] != 0.0 || !qs_finite(t[0])) scalars[SC_FLAG_NONFINITE] = 1.0;
   });
@@ -861,8 +861,8 @@ __global__ void __launch_bounds__(QS_THREADS) k_dot(int m, const double* a, cons
                                                     GridRed gr) {
   double v[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) v[0] += a[i] * b[i];
-  const RedOps<1> ops = {{RED_SUM}};
-  qs_grid_reduce<1>(v, ops, gr, [=](double (&t)[1]) { *out = t[0] * scale; });
+  using Ops = RedOps<RED_SUM>;
+  qs_grid_reduce<Ops>(v, gr, [=](double (&t)[1]) { *out = t[0] * scale; });
 }
 
 int vec_grid(i64 n) {

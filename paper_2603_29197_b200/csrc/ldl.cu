@@ -368,10 +368,27 @@ __global__ void __launch_bounds__(LDL_THREADS)
 // C(i, j) -= sum_k A(i, k) d_k A(j, k) over 64 x 64 tiles of the lower triangle.
 //   PANEL mode: C = panel columns [kb+nb, ns), rows [col, nr); k in [kb, kb+nb)
 //   SCHUR mode: C = U (nu x nu);                              k in [0, ns)
+// Inner product on the fp64 tensor pipe: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4; 37 TFLOP/s measured on B200,
+// tests/probes/dmma_probe.cu -- the same peak as DFMA, at an eighth of the issue slots and a quarter of the
+// shared-memory operand traffic).  8 warps as 2 x 4; a warp owns 32 x 16 of the tile = 4 x 2 DMMA blocks.
+// k-blocks of 32 are staged in shared memory [k][row] with a row stride of 68 doubles (= 4 mod 16: within each
+// half-warp the four k rows of a fragment fall on disjoint banks, so a fragment load is the minimal two wavefronts);
+// the next k-block is fetched into registers while the current one is multiplied.
+#define TSP (TS + 4)
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 template <bool SCHUR>
-__global__ void __launch_bounds__(LDL_THREADS)
-    k_blk_update(DevSym S, const int* list, int kb, double* L, double* U, const double* Dg) {
-  const int s = list[blockIdx.y];
+__global__ void __launch_bounds__(LDL_THREADS, 3)
+    k_blk_update(DevSym S, const int* list, const TileItem* tiles, int kb, double* L, double* U, const double* Dg) {
+  // SCHUR mode runs over an exact tile list built at analysis (no empty CTAs); PANEL mode keeps the lockstep grid
+  TileItem item{0, 0, 0};
+  if (SCHUR) item = tiles[blockIdx.x];
+  const int s = SCHUR ? item.front : list[blockIdx.y];
   const Front f = front_of(S, s, L, U);
   int k_lo, k_hi, c_lo, c_hi;
   if (SCHUR) {
@@ -389,63 +406,93 @@ __global__ void __launch_bounds__(LDL_THREADS)
   if (c_lo >= c_hi || k_lo >= k_hi) return;
   const int ntj = (c_hi - c_lo + TS - 1) / TS;
   const int nti = (f.nr - c_lo + TS - 1) / TS;
-  if ((int)blockIdx.x >= nti * ntj) return;
-  const int tj = blockIdx.x / nti, ti = blockIdx.x % nti;
+  if (!SCHUR && (int)blockIdx.x >= nti * ntj) return;
+  const int tj = SCHUR ? item.tj : blockIdx.x / nti, ti = SCHUR ? item.ti : blockIdx.x % nti;
   const int i0 = c_lo + ti * TS, j0 = c_lo + tj * TS;  // front-local row / column of the tile origin
   if (i0 + TS <= j0) return;                         // entirely above the diagonal
   const i64 nr = f.nr;
-  __shared__ double As[NB][TS + 2];
-  __shared__ double Bs[NB][TS + 2];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
-  double acc[4][4];
+  __shared__ double As[NB][TSP];
+  __shared__ double Bs[NB][TSP];
+  __shared__ double dsm[NB];  // pivots of the current k-block
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wi = 32 * (warp & 1), wj = 16 * (warp >> 1);
+  const int g = lane >> 2, t = lane & 3;
+  // a warp whose 32 x 16 block lies outside the front or strictly above the diagonal only helps with the staging
+  // (edge tiles of a 390-row update matrix hold 6 useful rows: most of their warps have nothing to multiply)
+  const bool live = (i0 + wi < f.nr) && (j0 + wj < c_hi) && (i0 + wi + 31 >= j0 + wj);
+  double acc[4][2][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int k0 = k_lo; k0 < k_hi; k0 += NB) {
+    for (int b2 = 0; b2 < 2; ++b2) acc[a][b2][0] = acc[a][b2][1] = 0.0;
+  // staging map: element e = tid + 256 u  ->  row r = e % 64 (consecutive threads, consecutive rows), k = e / 64
+  const int sr = tid & 63, sk = tid >> 6;  // k = sk + 4 u
+  // fetch() only ISSUES loads (raw values into registers, no arithmetic on them), so that they stay in flight
+  // across the multiply of the current k-block; the pivot scaling d_k is applied when a B fragment is read
+  double ra[8], rb[8], rd = 0.0;
+  auto fetch = [&](int k0) {
     const int kn = min(NB, k_hi - k0);
-    // stage A(i0.., k0..) and d_k * A(j0.., k0..): consecutive threads read consecutive rows (coalesced)
-    for (int e = tid; e < NB * TS; e += blockDim.x) {
-      const int r = e % TS, k = e / TS;
-      const int gi = i0 + r, gj = j0 + r;
-      double va = 0.0, vb = 0.0;
-      if (k < kn) {
-        if (gi < f.nr) va = f.Lp[gi + (i64)(k0 + k) * nr];
-        if (gj < c_hi) vb = f.Lp[gj + (i64)(k0 + k) * nr] * Dg[f.c0 + k0 + k];
-      }
-      As[k][r] = va;
-      Bs[k][r] = vb;
+    const int gi = i0 + sr, gj = j0 + sr;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = sk + 4 * u;
+      const bool ka = k < kn && gi < f.nr, kb2 = k < kn && gj < c_hi;
+      ra[u] = ka ? f.Lp[gi + (i64)(k0 + k) * nr] : 0.0;
+      rb[u] = kb2 ? f.Lp[gj + (i64)(k0 + k) * nr] : 0.0;
     }
-    __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < NB; ++k) {
-      double av[4], bv[4];
+    if (tid < NB) rd = tid < kn ? Dg[f.c0 + k0 + tid] : 0.0;
+  };
+  auto stage = [&]() {
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = As[k][tx + 16 * a];
+    for (int u = 0; u < 8; ++u) {
+      As[sk + 4 * u][sr] = ra[u];
+      Bs[sk + 4 * u][sr] = rb[u];
+    }
+    if (tid < NB) dsm[tid] = rd;
+  };
+  fetch(k_lo);
+  stage();
+  __syncthreads();
+  for (int k0 = k_lo; k0 < k_hi; k0 += NB) {
+    const bool more = k0 + NB < k_hi;
+    if (more) fetch(k0 + NB);  // in flight during the multiply below
+    if (live)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = Bs[k][ty + 16 * b];
+    for (int kk = 0; kk < NB; kk += 4) {
+      double av[4], bv[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kk + t][wi + 8 * a + g];
+#pragma unroll
+      for (int b2 = 0; b2 < 2; ++b2) bv[b2] = Bs[kk + t][wj + 8 * b2 + g] * dsm[kk + t];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
+        for (int b2 = 0; b2 < 2; ++b2) dmma_8x8x4(acc[a][b2], av[a], bv[b2]);
     }
     __syncthreads();
-  }
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int gj = j0 + ty + 16 * b;
-    if (gj >= c_hi) continue;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int gi = i0 + tx + 16 * a;
-      if (gi >= f.nr || gi < gj) continue;
-      if (SCHUR)
-        f.Up[(gi - f.ns) + (i64)(gj - f.ns) * f.nu] -= acc[a][b];
-      else
-        f.Lp[gi + (i64)gj * nr] -= acc[a][b];
+    if (more) {
+      stage();
+      __syncthreads();
     }
   }
+  // accumulator (a, b2, h) is C(i0 + wi + 8a + g, j0 + wj + 8 b2 + 2t + h)
+  if (!live) return;
+#pragma unroll
+  for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gj = j0 + wj + 8 * b2 + 2 * t + h;
+      if (gj >= c_hi) continue;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int gi = i0 + wi + 8 * a + g;
+        if (gi >= f.nr || gi < gj) continue;
+        if (SCHUR)
+          f.Up[(gi - f.ns) + (i64)(gj - f.ns) * f.nu] -= acc[a][b2][h];
+        else
+          f.Lp[gi + (i64)gj * nr] -= acc[a][b2][h];
+      }
+    }
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_zero_cb(DevSym S, const int* list, double* B) {
@@ -757,6 +804,23 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
     pmax = std::max(pmax, at);
   }
   d_poff = upload(poff, &owned, &device_bytes, st);
+  {
+    std::vector<TileItem> tiles;
+    tileptr.assign(S.nlevels + 1, 0);
+    for (int lv = 0; lv < S.nlevels; ++lv) {
+      for (int k = blkptr[lv]; k < blkptr[lv + 1]; ++k) {
+        const int fs = blk[k];
+        const int nu = (int)(S.rowptr[fs + 1] - S.rowptr[fs]) - (S.col0[fs + 1] - S.col0[fs]);
+        const int nt = (nu + TS - 1) / TS;
+        for (int tj = 0; tj < nt; ++tj)
+          for (int ti = tj; ti < nt; ++ti) tiles.push_back(TileItem{fs, (short)ti, (short)tj});
+      }
+      tileptr[lv + 1] = (i64)tiles.size();
+    }
+    d_tiles = upload(tiles, &owned, &device_bytes, st);
+    if (!d_tiles) return "cudaMalloc failed for the Schur tile list";
+    cudaStreamSynchronize(st);
+  }
   if (cudaMalloc((void**)&partial, std::max<i64>(pmax, 1) * 8) != cudaSuccess) return "cudaMalloc failed (solve partials)";
   owned.push_back(partial);
   device_bytes += pmax * 8;
@@ -939,15 +1003,15 @@ void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
         if (cols_left > 0) {
           const int ntj = (cols_left + TS - 1) / TS, nti = (mx_nr - kb - 1 + TS - 1) / TS;
           dim3 gu(ntj * nti, nb_fronts);
-          k_blk_update<false><<<gu, LDL_THREADS, 0, st>>>(D, lst, kb, L, U, Dg);
+          k_blk_update<false><<<gu, LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, L, U, Dg);
         }
       }
-      const int mx_nu = blk_max_nu[lv];
-      if (mx_nu > 0) {
-        const int nt = (mx_nu + TS - 1) / TS;
-        dim3 gu(nt * nt, nb_fronts);
-        k_blk_update<true><<<gu, LDL_THREADS, 0, st>>>(D, lst, 0, L, U, Dg);
-      }
+    }
+    // Schur complements of the level's blocked fronts: exact tile list
+    const i64 ntile = tileptr[lv + 1] - tileptr[lv];
+    for (i64 t0 = 0; t0 < ntile; t0 += (i64)1 << 30) {
+      const unsigned cnt2 = (unsigned)std::min<i64>((i64)1 << 30, ntile - t0);
+      k_blk_update<true><<<cnt2, LDL_THREADS, 0, st>>>(D, nullptr, d_tiles + tileptr[lv] + t0, 0, L, U, Dg);
     }
   }
 }

@@ -62,6 +62,11 @@ struct AsmLists {
   const i64* bandptr;     // [nsup+1] offsets into bandstart (only children of banded fronts have entries)
   const int* bandstart;
 };
+// Schur-complement work item: 64 x 64 tile (ti, tj), ti >= tj, of the update matrix of front `front`
+struct TileItem {
+  int front;
+  short ti, tj;
+};
 // extend-add work item of the list-driven kernel: column slot + row band (band = -1: whole column)
 struct EaItem {
   int slot, band;
@@ -92,6 +97,8 @@ struct LinSys {
   std::vector<int> genptr, slabptr, smallptr, blkptr, blk_max_ns, blk_max_nr, blk_max_nu;
   AsmLists A{};
   EaItem* d_eaitems = nullptr;
+  TileItem* d_tiles = nullptr;      // Schur tiles of the blocked fronts, level by level
+  std::vector<i64> tileptr;         // [nlevels+1]
   std::vector<i64> lvslot, eaptr;   // per level: slot range, extend-add item range
   std::vector<int> lv_tpr;          // per level: lanes per slot in the forward-solve gather
   bool use_lists = true;

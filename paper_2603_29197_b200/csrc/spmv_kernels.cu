@@ -69,8 +69,94 @@ __device__ __forceinline__ void row_dot4(const Csr& M, const int (&row)[4], cons
   }
 }
 
+// Short rows (a handful of entries): one thread per row, plain loop.  Few instructions and few registers, so
+// many warps are resident and their load chains overlap; the generic lane-group machinery costs ~10x more
+// instructions per entry on such rows.  Same summation order as a one-lane group.
+__device__ __forceinline__ double row_dot_thread(const Csr& M, int row, const double* __restrict__ x) {
+  double acc = 0.0;
+  const int e = M.ptr[row + 1];
+  for (int p = M.ptr[row]; p < e; ++p) acc += M.val[p] * x[M.idx[p]];
+  return acc;
+}
+
+// The dual range needs three products per row (P x, A'y, G'z).  Run them side by side: NM matrices x NR rows =
+// NM * NR independent load chains (row pointer -> index/value -> operand) per lane group, so a trip costs three
+// dependent memory round trips instead of nine.
+template <int NM, int NR>
+__device__ __forceinline__ void row_dots(const Csr* const (&M)[NM], const double* const (&x)[NM], const int (&row)[NR],
+                                         int lane, int tpr, unsigned mask, double (&acc)[NM][NR]) {
+  int b[NM][NR], e[NM][NR];
+#pragma unroll
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const bool ok = row[r] < M[m]->rows;
+      b[m][r] = ok ? M[m]->ptr[row[r]] + lane : 0;
+      e[m][r] = ok ? M[m]->ptr[row[r] + 1] : 0;
+      acc[m][r] = 0.0;
+    }
+  bool more = true;
+  while (more) {
+    more = false;
+    int ix[NM][NR];
+    double va[NM][NR];
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const bool on = b[m][r] < e[m][r];
+        ix[m][r] = on ? M[m]->idx[b[m][r]] : 0;
+        va[m][r] = on ? M[m]->val[b[m][r]] : 0.0;
+      }
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (b[m][r] < e[m][r]) {
+          acc[m][r] += va[m][r] * x[m][ix[m][r]];
+          b[m][r] += tpr;
+          more |= b[m][r] < e[m][r];
+        }
+      }
+  }
+  for (int o = tpr >> 1; o > 0; o >>= 1) {
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) acc[m][r] += __shfl_xor_sync(mask, acc[m][r], o);
+  }
+}
+
 __device__ __forceinline__ unsigned lane_mask(int tpr) {
   return tpr == 32 ? 0xffffffffu : (((1u << tpr) - 1u) << (threadIdx.x & 31 & ~(tpr - 1)));
+}
+
+// Long rows (mean length >= 512, e.g. the 2000-entry rows of a design matrix): the whole CTA takes one row,
+// 4 independent loads in flight per thread, fixed-order block reduction.  Every thread gets the sum.
+#define QS_TPR_CTA 256
+__device__ __forceinline__ double row_dot_cta(const Csr& M, int row, const double* __restrict__ x, double* sm /*[8]*/) {
+  const int b = M.ptr[row], e = M.ptr[row + 1];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int p = b + threadIdx.x;
+  for (; p + 3 * QS_THREADS < e; p += 4 * QS_THREADS) {
+    const int i0 = M.idx[p], i1 = M.idx[p + QS_THREADS], i2 = M.idx[p + 2 * QS_THREADS], i3 = M.idx[p + 3 * QS_THREADS];
+    const double v0 = M.val[p], v1 = M.val[p + QS_THREADS], v2 = M.val[p + 2 * QS_THREADS], v3 = M.val[p + 3 * QS_THREADS];
+    a0 += v0 * x[i0];
+    a1 += v1 * x[i1];
+    a2 += v2 * x[i2];
+    a3 += v3 * x[i3];
+  }
+  for (; p < e; p += QS_THREADS) a0 += M.val[p] * x[M.idx[p]];
+  double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __syncthreads();  // sm may still be read from the previous row
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < QS_THREADS / 32; ++w) t += sm[w];
+  return t;
 }
 
 struct RowRange {
@@ -79,25 +165,33 @@ struct RowRange {
   unsigned mask;
 };
 
-// block ranges: nbd blocks stride over the dual rows, nbe over the eq rows, the
-// rest over the cone rows; a group of tpr lanes owns a row
+// block ranges: the first nbe blocks stride over the eq rows (rows of A are the long ones when A is a design
+// matrix: start them first), the next nbd over the dual rows, the rest over the cone rows; a group of tpr lanes
+// owns a row (tpr == QS_TPR_CTA: the whole CTA)
 __device__ __forceinline__ RowRange locate(int nbd, int nbe, int nbc, int tpr_d, int tpr_e, int tpr_c) {
   RowRange r;
   int b = blockIdx.x, nb;
-  if (b < nbd) {
-    r.which = 0;
-    r.tpr = tpr_d;
-    nb = nbd;
-  } else if (b < nbd + nbe) {
+  if (b < nbe) {
     r.which = 1;
     r.tpr = tpr_e;
-    b -= nbd;
     nb = nbe;
+  } else if (b < nbe + nbd) {
+    r.which = 0;
+    r.tpr = tpr_d;
+    b -= nbe;
+    nb = nbd;
   } else {
     r.which = 2;
     r.tpr = tpr_c;
     b -= nbd + nbe;
     nb = nbc;
+  }
+  if (r.tpr == QS_TPR_CTA) {
+    r.row = b;
+    r.stride = nb;
+    r.lane = threadIdx.x;
+    r.mask = 0xffffffffu;
+    return r;
   }
   r.row = (b * blockDim.x + threadIdx.x) / r.tpr;
   r.stride = nb * (QS_THREADS / r.tpr);
@@ -118,29 +212,63 @@ __global__ void __launch_bounds__(QS_THREADS)
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = 0.0;
   const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
-  if (r.which == 0) {
-    for (int row0 = r.row; row0 < A.n; row0 += 4 * r.stride) {
-      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
-      double px[4], aty[4], gtz[4];
-      row_dot4(A.Pf, rows, A.x, r.lane, r.tpr, r.mask, px);
-      row_dot4(A.At, rows, A.y, r.lane, r.tpr, r.mask, aty);
-      row_dot4(A.Gt, rows, A.z, r.lane, r.tpr, r.mask, gtz);
+  if (r.which == 0 && r.tpr == 1) {
+    for (int row = r.row; row < A.n; row += r.stride) {
+      const double px = row_dot_thread(A.Pf, row, A.x), aty = row_dot_thread(A.At, row, A.y),
+                   gtz = row_dot_thread(A.Gt, row, A.z);
+      const double ci = A.c[row], xi = A.x[row];
+      const double rd = px + ci + aty + gtz;  // ipm.py:76
+      A.rhs[row] = -rd;
+      v[PX] = absmax(v[PX], px);
+      v[ATY] = absmax(v[ATY], aty);
+      v[GTZ] = absmax(v[GTZ], gtz);
+      v[RD] = absmax(v[RD], rd);
+      v[XPX] += xi * px;
+      v[CX] += ci * xi;
+    }
+  } else if (r.which == 0) {
+    const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
+    const double* const vecs[3] = {A.x, A.y, A.z};
+    for (int row0 = r.row; row0 < A.n; row0 += 2 * r.stride) {
+      const int rows[2] = {row0, row0 + r.stride};
+      double d[3][2];
+      row_dots<3, 2>(mats, vecs, rows, r.lane, r.tpr, r.mask, d);
       if (r.lane == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const int row = rows[q];
           if (row >= A.n) continue;
+          const double px = d[0][q], aty = d[1][q], gtz = d[2][q];
           const double ci = A.c[row], xi = A.x[row];
-          const double rd = px[q] + ci + aty[q] + gtz[q];  // ipm.py:76
+          const double rd = px + ci + aty + gtz;  // ipm.py:76
           A.rhs[row] = -rd;
-          v[PX] = absmax(v[PX], px[q]);
-          v[ATY] = absmax(v[ATY], aty[q]);
-          v[GTZ] = absmax(v[GTZ], gtz[q]);
+          v[PX] = absmax(v[PX], px);
+          v[ATY] = absmax(v[ATY], aty);
+          v[GTZ] = absmax(v[GTZ], gtz);
           v[RD] = absmax(v[RD], rd);
-          v[XPX] += xi * px[q];
+          v[XPX] += xi * px;
           v[CX] += ci * xi;
         }
       }
+    }
+  } else if (r.which == 1 && r.tpr == QS_TPR_CTA) {
+    __shared__ double rsm[QS_THREADS / 32];
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double ax = row_dot_cta(A.Ar, row, A.x, rsm);
+      if (threadIdx.x == 0) {
+        const double re = ax - A.b[row];  // ipm.py:77
+        A.rhs[A.n + row] = -re;
+        v[AX] = absmax(v[AX], ax);
+        v[RE] = absmax(v[RE], re);
+      }
+    }
+  } else if (r.which == 1 && r.tpr == 1) {
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double ax = row_dot_thread(A.Ar, row, A.x);
+      const double re = ax - A.b[row];  // ipm.py:77
+      A.rhs[A.n + row] = -re;
+      v[AX] = absmax(v[AX], ax);
+      v[RE] = absmax(v[RE], re);
     }
   } else if (r.which == 1) {
     for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
@@ -158,6 +286,31 @@ __global__ void __launch_bounds__(QS_THREADS)
           v[RE] = absmax(v[RE], re);
         }
       }
+    }
+  } else if (r.tpr == QS_TPR_CTA) {
+    __shared__ double rsm2[QS_THREADS / 32];
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const double gx = row_dot_cta(A.Gr, row, A.x, rsm2);
+      if (threadIdx.x == 0) {
+        const double si = A.s[row];
+        const double rc = gx + si - A.h[row];  // ipm.py:78
+        A.r_cone[row] = rc;
+        v[GX] = absmax(v[GX], gx);
+        v[SN] = absmax(v[SN], si);
+        v[RC] = absmax(v[RC], rc);
+        v[GAP] += si * A.z[row];
+      }
+    }
+  } else if (r.tpr == 1) {
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const double gx = row_dot_thread(A.Gr, row, A.x);
+      const double si = A.s[row];
+      const double rc = gx + si - A.h[row];  // ipm.py:78
+      A.r_cone[row] = rc;
+      v[GX] = absmax(v[GX], gx);
+      v[SN] = absmax(v[SN], si);
+      v[RC] = absmax(v[RC], rc);
+      v[GAP] += si * A.z[row];
     }
   } else {
     for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
@@ -180,10 +333,10 @@ __global__ void __launch_bounds__(QS_THREADS)
       }
     }
   }
-  const RedOps<NV> ops = {{RED_MAX, RED_MAX, RED_MAX, RED_MAX, RED_SUM, RED_SUM, RED_MAX, RED_MAX, RED_MAX, RED_MAX,
-                           RED_MAX, RED_SUM}};
+  using Ops = RedOps<RED_AMAX, RED_AMAX, RED_AMAX, RED_AMAX, RED_SUM, RED_SUM, RED_AMAX, RED_AMAX, RED_AMAX, RED_AMAX,
+                     RED_AMAX, RED_SUM>;  // every max here is over |x| values
   double* sc = A.scalars;
-  qs_grid_reduce<NV>(v, ops, A.gr, [=](double (&t)[NV]) {
+  qs_grid_reduce<Ops>(v, A.gr, [=](double (&t)[NV]) {
     sc[SC_NORM_PX] = t[PX];
     sc[SC_NORM_ATY] = t[ATY];
     sc[SC_NORM_GTZ] = t[GTZ];
@@ -215,22 +368,45 @@ __global__ void __launch_bounds__(QS_THREADS)
   const double* vx = A.v;
   const double* vy = A.v + A.n;
   const double* vz = A.v + A.n + A.p;
-  if (r.which == 0) {
-    for (int row0 = r.row; row0 < A.n; row0 += 4 * r.stride) {
-      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
-      double px[4], aty[4], gtz[4];
-      row_dot4(A.Pf, rows, vx, r.lane, r.tpr, r.mask, px);
-      row_dot4(A.At, rows, vy, r.lane, r.tpr, r.mask, aty);
-      row_dot4(A.Gt, rows, vz, r.lane, r.tpr, r.mask, gtz);
+  if (r.which == 0 && r.tpr == 1) {
+    for (int row = r.row; row < A.n; row += r.stride) {
+      const double t = A.rhs[row] - (row_dot_thread(A.Pf, row, vx) + row_dot_thread(A.At, row, vy) +
+                                     row_dot_thread(A.Gt, row, vz));
+      A.r[row] = t;
+      v[0] = absmax(v[0], t);
+    }
+  } else if (r.which == 0) {
+    const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
+    const double* const vecs[3] = {vx, vy, vz};
+    for (int row0 = r.row; row0 < A.n; row0 += 2 * r.stride) {
+      const int rows[2] = {row0, row0 + r.stride};
+      double d[3][2];
+      row_dots<3, 2>(mats, vecs, rows, r.lane, r.tpr, r.mask, d);
       if (r.lane == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           if (rows[q] >= A.n) continue;
-          const double t = A.rhs[rows[q]] - (px[q] + aty[q] + gtz[q]);
+          const double t = A.rhs[rows[q]] - (d[0][q] + d[1][q] + d[2][q]);
           A.r[rows[q]] = t;
           v[0] = absmax(v[0], t);
         }
       }
+    }
+  } else if (r.which == 1 && r.tpr == QS_TPR_CTA) {
+    __shared__ double rsm[QS_THREADS / 32];
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double ax = row_dot_cta(A.Ar, row, vx, rsm);
+      if (threadIdx.x == 0) {
+        const double t = A.rhs[A.n + row] - ax;
+        A.r[A.n + row] = t;
+        v[0] = absmax(v[0], t);
+      }
+    }
+  } else if (r.which == 1 && r.tpr == 1) {
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double t = A.rhs[A.n + row] - row_dot_thread(A.Ar, row, vx);
+      A.r[A.n + row] = t;
+      v[0] = absmax(v[0], t);
     }
   } else if (r.which == 1) {
     for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
@@ -246,6 +422,24 @@ __global__ void __launch_bounds__(QS_THREADS)
           v[0] = absmax(v[0], t);
         }
       }
+    }
+  } else if (r.tpr == QS_TPR_CTA) {
+    __shared__ double rsm2[QS_THREADS / 32];
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const double gx = row_dot_cta(A.Gr, row, vx, rsm2);
+      if (threadIdx.x == 0) {
+        const int i = A.n + A.p + row;
+        const double t = A.rhs[i] - (gx - A.w2vz[row]);
+        A.r[i] = t;
+        v[0] = absmax(v[0], t);
+      }
+    }
+  } else if (r.tpr == 1) {
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const int i = A.n + A.p + row;
+      const double t = A.rhs[i] - (row_dot_thread(A.Gr, row, vx) - A.w2vz[row]);
+      A.r[i] = t;
+      v[0] = absmax(v[0], t);
     }
   } else {
     for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
@@ -264,13 +458,21 @@ __global__ void __launch_bounds__(QS_THREADS)
       }
     }
   }
-  const RedOps<1> ops = {{RED_MAX}};
+  using Ops = RedOps<RED_AMAX>;
   double* out = A.scalars + A.slot;
-  qs_grid_reduce<1>(v, ops, A.gr, [=](double (&t)[1]) { *out = t[0]; });
+  qs_grid_reduce<Ops>(v, A.gr, [=](double (&t)[1]) { *out = t[0]; });
 }
 
 // plain y (+)= M x, gather form
 __global__ void __launch_bounds__(QS_THREADS) k_spmv_csr(Csr M, const double* x, double* y, int accumulate) {
+  if (M.tpr == QS_TPR_CTA) {
+    __shared__ double rsm[QS_THREADS / 32];
+    for (int row = blockIdx.x; row < M.rows; row += gridDim.x) {
+      const double d = row_dot_cta(M, row, x, rsm);
+      if (threadIdx.x == 0) y[row] = accumulate ? y[row] + d : d;
+    }
+    return;
+  }
   const int tpr = M.tpr;
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / tpr;
   const double d = row_dot(M, row, x, threadIdx.x & (tpr - 1), tpr, lane_mask(tpr));
@@ -308,8 +510,8 @@ __global__ void __launch_bounds__(QS_THREADS) k_absmax(i64 n, const double* x, d
   double v[1] = {0.0};
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
     v[0] = absmax(v[0], x[i]);
-  const RedOps<1> ops = {{RED_MAX}};
-  qs_grid_reduce<1>(v, ops, gr, [=](double (&t)[1]) {
+  using Ops = RedOps<RED_AMAX>;
+  qs_grid_reduce<Ops>(v, gr, [=](double (&t)[1]) {
     *out = t[0];
     if (nonfinite && !qs_finite(t[0])) *nonfinite = 1.0;
   });
@@ -317,13 +519,17 @@ __global__ void __launch_bounds__(QS_THREADS) k_absmax(i64 n, const double* x, d
 
 int blocks_for(int rows, int tpr) {
   if (rows <= 0) return 0;
+  if (tpr == QS_TPR_CTA) return rows > QS_MAX_GRID ? QS_MAX_GRID : rows;
   const int rpb = QS_THREADS / tpr;
   return (rows + rpb - 1) / rpb;
 }
 
-int blocks_capped(int rows, int tpr) {
-  // a lane group takes 4 rows per trip; enough blocks that most groups make one trip
-  const int b = blocks_for((rows + 3) / 4, tpr), cap = QS_MAX_GRID / 4;
+int blocks_capped(int rows, int tpr, int rows_per_trip = 4) {
+  // a lane group takes 4 rows per trip; at most 8 blocks per SM and range, so that on large problems every
+  // group makes several trips and the 12-value block reduction at the end is amortised
+  if (tpr == QS_TPR_CTA) return blocks_for(rows, tpr);
+  if (tpr == 1) rows_per_trip = 1;  // thread-per-row path
+  const int b = blocks_for((rows + rows_per_trip - 1) / rows_per_trip, tpr), cap = 148 * 8;
   return b > cap ? cap : b;
 }
 
@@ -339,18 +545,20 @@ int vgrid(i64 n) {
 int qsk_pick_tpr(i64 nnz, i64 rows) {
   if (rows <= 0) return 1;
   const double mean = (double)nnz / (double)rows;
+  if (mean >= 512.0) return QS_TPR_CTA;  // long rows: a CTA per row
+  if (mean <= 6.0) return 1;             // short rows: a thread per row
   int t = 1;
   while (t < 32 && t * 2 <= mean) t <<= 1;  // largest power of two <= mean row length
   return t;
 }
 
 void qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
-  const int nbd = blocks_capped(A.n, A.Pf.tpr), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
+  const int nbd = blocks_capped(A.n, A.Pf.tpr, 2), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
   k_residuals<<<nbd + nbe + nbc, QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
 }
 
 void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st) {
-  const int nbd = blocks_capped(A.n, A.Pf.tpr), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
+  const int nbd = blocks_capped(A.n, A.Pf.tpr, 2), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
   k_kkt_residual<<<nbd + nbe + nbc, QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
 }
 

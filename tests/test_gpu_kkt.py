@@ -91,3 +91,34 @@ def test_spmv_vs_reference_golden(name):
     ref = g["K_times_vec"]
     assert np.allclose(out.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.max(np.abs(ref)))
     lib.qs_destroy(h)
+
+
+def test_spmv_long_rows_cta_per_row():
+    """Rows of >= 512 entries on average take the CTA-per-row path of the gather products (spmv_kernels.cu)."""
+    import scipy.sparse as sp
+    import torch
+
+    rng = np.random.default_rng(5)
+    rows, cols = 37, 6000
+    S = sp.random(rows, cols, density=0.15, random_state=7, format="csr", dtype=np.float64)  # ~900 per row
+    S.sort_indices()
+    x = rng.standard_normal(cols)
+    lib = _lib.require_device(0)
+    h = lib.qs_create(0)
+    dev = torch.device("cuda", 0)
+    ptr = torch.as_tensor(S.indptr.astype(np.int32)).to(dev)
+    idx = torch.as_tensor(S.indices.astype(np.int32)).to(dev)
+    val = torch.as_tensor(S.data).to(dev)
+    xd = torch.as_tensor(x).to(dev)
+    y = torch.ones(rows, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    for accumulate, base in ((0, 0.0), (1, 1.0)):
+        y.fill_(1.0)
+        torch.cuda.synchronize()
+        rc = lib.qs_spmv_csr(h, rows, cols, C.c_void_p(ptr.data_ptr()), C.c_void_p(idx.data_ptr()),
+                             C.c_void_p(val.data_ptr()), C.c_void_p(xd.data_ptr()), C.c_void_p(y.data_ptr()), accumulate)
+        _lib.check(lib, h, rc)
+        lib.qs_sync(h)
+        ref = S @ x + base
+        assert np.allclose(y.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.max(np.abs(ref)))
+    lib.qs_destroy(h)

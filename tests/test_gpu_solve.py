@@ -208,3 +208,17 @@ def test_device_assembled_kkt_is_bit_exact(name, monkeypatch):
         assert np.array_equal(np.signbit(got.matrix.values), np.signbit(ref.matrix.values))
         assert np.array_equal(got.nt_entry_positions, ref.nt_entry_positions)
         dev.close()
+
+
+def test_solve_with_long_design_rows_matches_oracle(oracle):
+    """A group-lasso instance whose equality rows hold ~800 entries each: the residual and refinement kernels take
+    their CTA-per-row path; iterations and objective must still match the CPU oracle."""
+    from paper_2603_29197_b200 import configs
+
+    d = configs.group_lasso(groups=40, qlo=20, qhi=250, samples=20, nnz_per_col=3, seed=5)
+    assert d.A.nnz / d.p >= 512
+    res = run(d)
+    ref = oracle.solve(d)
+    assert res.status.value == ref.status == "Solved"
+    assert abs(res.iterations - ref.iterations) <= 1
+    assert abs(res.objective - ref.objective) <= 1e-6 * max(1.0, abs(ref.objective))
