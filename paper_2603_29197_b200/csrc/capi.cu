@@ -1035,9 +1035,8 @@ int qs_residuals(qs_handle* h, qs_residual_info* out) {
   h->tm.begin(T_RESID, h->stream);
   ResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->x, h->y, h->z, h->s,
                  h->c,      h->b,      h->hv,     h->rhs, h->r_cone, h->scalars, h->gr};
-  qsk_residuals(A, h->stream);
+  h->launches += qsk_residuals(A, h->stream);
   h->tm.end(h->stream);
-  h->launches++;
   int rc = check_launch(h, "residuals");
   if (rc) return rc;
   rc = fetch_scalars(h);

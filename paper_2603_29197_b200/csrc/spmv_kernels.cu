@@ -16,6 +16,8 @@
 // [dual | eq | cone] with all norms reduced in the same pass.
 #include "spmv_kernels.h"
 
+#include <algorithm>
+
 namespace {
 
 __device__ __forceinline__ double row_dot(const Csr& M, int row, const double* __restrict__ x, int lane, int tpr,
@@ -205,28 +207,53 @@ __device__ __forceinline__ double absmax(double a, double v) {
   return (t > a || t != t) ? t : a;  // NaN sticks
 }
 
-__global__ void __launch_bounds__(QS_THREADS)
-    k_residuals(ResidualArgs A, int nbd, int nbe, int nbc) {
-  enum { PX, ATY, GTZ, RD, XPX, CX, AX, RE, GX, SN, RC, GAP, NV };
+// compute_residuals is three launches, one per row range (dual / eq / cone), each compiled for ONE row-product
+// mode: a fused single kernel carried the registers of all nine (range, mode) paths (80 per thread, 3 CTAs per
+// SM) and, with rows this short, the kernel is bound by how many load chains are in flight.
+enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2 };
+enum { RANGE_DUAL = 0, RANGE_EQ = 1, RANGE_CONE = 2 };
+
+__device__ __forceinline__ RowRange locate1(int tpr, int mode) {
+  RowRange r;
+  r.which = 0;
+  r.tpr = tpr;
+  if (mode == MODE_CTA) {
+    r.row = blockIdx.x;
+    r.stride = gridDim.x;
+    r.lane = threadIdx.x;
+    r.mask = 0xffffffffu;
+    return r;
+  }
+  r.row = (blockIdx.x * blockDim.x + threadIdx.x) / tpr;
+  r.stride = gridDim.x * (QS_THREADS / tpr);
+  r.lane = threadIdx.x & (tpr - 1);
+  r.mask = lane_mask(tpr);
+  return r;
+}
+
+// r_dual = P x + c + A'y + G'z (ipm.py:76), -r_dual -> rhs[0:n]; |Px|, |A'y|, |G'z|, |r_dual| (inf norms), x'Px, c'x
+template <int MODE>
+__global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
+  enum { PX, ATY, GTZ, RD, XPX, CX, NV };
   double v[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = 0.0;
-  const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
-  if (r.which == 0 && r.tpr == 1) {
-    for (int row = r.row; row < A.n; row += r.stride) {
-      const double px = row_dot_thread(A.Pf, row, A.x), aty = row_dot_thread(A.At, row, A.y),
-                   gtz = row_dot_thread(A.Gt, row, A.z);
-      const double ci = A.c[row], xi = A.x[row];
-      const double rd = px + ci + aty + gtz;  // ipm.py:76
-      A.rhs[row] = -rd;
-      v[PX] = absmax(v[PX], px);
-      v[ATY] = absmax(v[ATY], aty);
-      v[GTZ] = absmax(v[GTZ], gtz);
-      v[RD] = absmax(v[RD], rd);
-      v[XPX] += xi * px;
-      v[CX] += ci * xi;
-    }
-  } else if (r.which == 0) {
+  const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Pf.tpr, MODE);
+  auto finish_row = [&](int row, double px, double aty, double gtz) {
+    const double ci = A.c[row], xi = A.x[row];
+    const double rd = px + ci + aty + gtz;
+    A.rhs[row] = -rd;
+    v[PX] = absmax(v[PX], px);
+    v[ATY] = absmax(v[ATY], aty);
+    v[GTZ] = absmax(v[GTZ], gtz);
+    v[RD] = absmax(v[RD], rd);
+    v[XPX] += xi * px;
+    v[CX] += ci * xi;
+  };
+  if (MODE == MODE_THREAD) {
+    for (int row = r.row; row < A.n; row += r.stride)
+      finish_row(row, row_dot_thread(A.Pf, row, A.x), row_dot_thread(A.At, row, A.y), row_dot_thread(A.Gt, row, A.z));
+  } else {
     const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
     const double* const vecs[3] = {A.x, A.y, A.z};
     for (int row0 = r.row; row0 < A.n; row0 += 2 * r.stride) {
@@ -235,107 +262,14 @@ __global__ void __launch_bounds__(QS_THREADS)
       row_dots<3, 2>(mats, vecs, rows, r.lane, r.tpr, r.mask, d);
       if (r.lane == 0) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int row = rows[q];
-          if (row >= A.n) continue;
-          const double px = d[0][q], aty = d[1][q], gtz = d[2][q];
-          const double ci = A.c[row], xi = A.x[row];
-          const double rd = px + ci + aty + gtz;  // ipm.py:76
-          A.rhs[row] = -rd;
-          v[PX] = absmax(v[PX], px);
-          v[ATY] = absmax(v[ATY], aty);
-          v[GTZ] = absmax(v[GTZ], gtz);
-          v[RD] = absmax(v[RD], rd);
-          v[XPX] += xi * px;
-          v[CX] += ci * xi;
-        }
-      }
-    }
-  } else if (r.which == 1 && r.tpr == QS_TPR_CTA) {
-    __shared__ double rsm[QS_THREADS / 32];
-    for (int row = r.row; row < A.p; row += r.stride) {
-      const double ax = row_dot_cta(A.Ar, row, A.x, rsm);
-      if (threadIdx.x == 0) {
-        const double re = ax - A.b[row];  // ipm.py:77
-        A.rhs[A.n + row] = -re;
-        v[AX] = absmax(v[AX], ax);
-        v[RE] = absmax(v[RE], re);
-      }
-    }
-  } else if (r.which == 1 && r.tpr == 1) {
-    for (int row = r.row; row < A.p; row += r.stride) {
-      const double ax = row_dot_thread(A.Ar, row, A.x);
-      const double re = ax - A.b[row];  // ipm.py:77
-      A.rhs[A.n + row] = -re;
-      v[AX] = absmax(v[AX], ax);
-      v[RE] = absmax(v[RE], re);
-    }
-  } else if (r.which == 1) {
-    for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
-      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
-      double ax[4];
-      row_dot4(A.Ar, rows, A.x, r.lane, r.tpr, r.mask, ax);
-      if (r.lane == 0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int row = rows[q];
-          if (row >= A.p) continue;
-          const double re = ax[q] - A.b[row];  // ipm.py:77
-          A.rhs[A.n + row] = -re;
-          v[AX] = absmax(v[AX], ax[q]);
-          v[RE] = absmax(v[RE], re);
-        }
-      }
-    }
-  } else if (r.tpr == QS_TPR_CTA) {
-    __shared__ double rsm2[QS_THREADS / 32];
-    for (int row = r.row; row < A.m; row += r.stride) {
-      const double gx = row_dot_cta(A.Gr, row, A.x, rsm2);
-      if (threadIdx.x == 0) {
-        const double si = A.s[row];
-        const double rc = gx + si - A.h[row];  // ipm.py:78
-        A.r_cone[row] = rc;
-        v[GX] = absmax(v[GX], gx);
-        v[SN] = absmax(v[SN], si);
-        v[RC] = absmax(v[RC], rc);
-        v[GAP] += si * A.z[row];
-      }
-    }
-  } else if (r.tpr == 1) {
-    for (int row = r.row; row < A.m; row += r.stride) {
-      const double gx = row_dot_thread(A.Gr, row, A.x);
-      const double si = A.s[row];
-      const double rc = gx + si - A.h[row];  // ipm.py:78
-      A.r_cone[row] = rc;
-      v[GX] = absmax(v[GX], gx);
-      v[SN] = absmax(v[SN], si);
-      v[RC] = absmax(v[RC], rc);
-      v[GAP] += si * A.z[row];
-    }
-  } else {
-    for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
-      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
-      double gx[4];
-      row_dot4(A.Gr, rows, A.x, r.lane, r.tpr, r.mask, gx);
-      if (r.lane == 0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int row = rows[q];
-          if (row >= A.m) continue;
-          const double si = A.s[row];
-          const double rc = gx[q] + si - A.h[row];  // ipm.py:78
-          A.r_cone[row] = rc;
-          v[GX] = absmax(v[GX], gx[q]);
-          v[SN] = absmax(v[SN], si);
-          v[RC] = absmax(v[RC], rc);
-          v[GAP] += si * A.z[row];
-        }
+        for (int q = 0; q < 2; ++q)
+          if (rows[q] < A.n) finish_row(rows[q], d[0][q], d[1][q], d[2][q]);
       }
     }
   }
-  using Ops = RedOps<RED_AMAX, RED_AMAX, RED_AMAX, RED_AMAX, RED_SUM, RED_SUM, RED_AMAX, RED_AMAX, RED_AMAX, RED_AMAX,
-                     RED_AMAX, RED_SUM>;  // every max here is over |x| values
+  using Ops = RedOps<RED_AMAX, RED_AMAX, RED_AMAX, RED_AMAX, RED_SUM, RED_SUM>;
   double* sc = A.scalars;
+  const int p = A.p;
   qs_grid_reduce<Ops>(v, A.gr, [=](double (&t)[NV]) {
     sc[SC_NORM_PX] = t[PX];
     sc[SC_NORM_ATY] = t[ATY];
@@ -344,14 +278,95 @@ __global__ void __launch_bounds__(QS_THREADS)
     sc[SC_XPX] = t[XPX];
     sc[SC_CX] = t[CX];
     sc[SC_OBJ] = 0.5 * t[XPX] + t[CX];
+    if (p == 0) sc[SC_NORM_AX] = sc[SC_NORM_REQ] = 0.0;  // no equality launch
+    if (!qs_finite(t[RD])) sc[SC_FLAG_NONFINITE] = 1.0;   // ipm.py:96-102
+  });
+}
+
+// r_eq = A x - b (ipm.py:77), -r_eq -> rhs[n:n+p]; |Ax|, |r_eq|
+template <int MODE>
+__global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
+  enum { AX, RE, NV };
+  double v[NV] = {0.0, 0.0};
+  const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Ar.tpr, MODE);
+  auto finish_row = [&](int row, double ax) {
+    const double re = ax - A.b[row];
+    A.rhs[A.n + row] = -re;
+    v[AX] = absmax(v[AX], ax);
+    v[RE] = absmax(v[RE], re);
+  };
+  if (MODE == MODE_THREAD) {
+    for (int row = r.row; row < A.p; row += r.stride) finish_row(row, row_dot_thread(A.Ar, row, A.x));
+  } else if (MODE == MODE_CTA) {
+    __shared__ double rsm[QS_THREADS / 32];
+    for (int row = r.row; row < A.p; row += r.stride) {
+      const double ax = row_dot_cta(A.Ar, row, A.x, rsm);
+      if (threadIdx.x == 0) finish_row(row, ax);
+    }
+  } else {
+    for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double ax[4];
+      row_dot4(A.Ar, rows, A.x, r.lane, r.tpr, r.mask, ax);
+      if (r.lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (rows[q] < A.p) finish_row(rows[q], ax[q]);
+      }
+    }
+  }
+  using Ops = RedOps<RED_AMAX, RED_AMAX>;
+  double* sc = A.scalars;
+  qs_grid_reduce<Ops>(v, A.gr, [=](double (&t)[NV]) {
     sc[SC_NORM_AX] = t[AX];
     sc[SC_NORM_REQ] = t[RE];
+    if (!qs_finite(t[RE])) sc[SC_FLAG_NONFINITE] = 1.0;
+  });
+}
+
+// r_cone = G x + s - h (ipm.py:78); |Gx|, |s|, |r_cone|, gap = s'z (ipm.py:79)
+template <int MODE>
+__global__ void __launch_bounds__(QS_THREADS) k_resid_cone(ResidualArgs A) {
+  enum { GX, SN, RC, GAP, NV };
+  double v[NV] = {0.0, 0.0, 0.0, 0.0};
+  const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Gr.tpr, MODE);
+  auto finish_row = [&](int row, double gx) {
+    const double si = A.s[row];
+    const double rc = gx + si - A.h[row];
+    A.r_cone[row] = rc;
+    v[GX] = absmax(v[GX], gx);
+    v[SN] = absmax(v[SN], si);
+    v[RC] = absmax(v[RC], rc);
+    v[GAP] += si * A.z[row];
+  };
+  if (MODE == MODE_THREAD) {
+    for (int row = r.row; row < A.m; row += r.stride) finish_row(row, row_dot_thread(A.Gr, row, A.x));
+  } else if (MODE == MODE_CTA) {
+    __shared__ double rsm[QS_THREADS / 32];
+    for (int row = r.row; row < A.m; row += r.stride) {
+      const double gx = row_dot_cta(A.Gr, row, A.x, rsm);
+      if (threadIdx.x == 0) finish_row(row, gx);
+    }
+  } else {
+    for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double gx[4];
+      row_dot4(A.Gr, rows, A.x, r.lane, r.tpr, r.mask, gx);
+      if (r.lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (rows[q] < A.m) finish_row(rows[q], gx[q]);
+      }
+    }
+  }
+  using Ops = RedOps<RED_AMAX, RED_AMAX, RED_AMAX, RED_SUM>;
+  double* sc = A.scalars;
+  qs_grid_reduce<Ops>(v, A.gr, [=](double (&t)[NV]) {
     sc[SC_NORM_GX] = t[GX];
     sc[SC_NORM_S] = t[SN];
     sc[SC_NORM_RCONE] = t[RC];
     sc[SC_GAP] = t[GAP];
-    if (!qs_finite(t[RD]) || !qs_finite(t[RE]) || !qs_finite(t[RC]) || !qs_finite(t[GAP]))
-      sc[SC_FLAG_NONFINITE] = 1.0;  // ipm.py:96-102
+    if (!qs_finite(t[RC]) || !qs_finite(t[GAP])) sc[SC_FLAG_NONFINITE] = 1.0;
   });
 }
 
@@ -552,9 +567,26 @@ int qsk_pick_tpr(i64 nnz, i64 rows) {
   return t;
 }
 
-void qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
-  const int nbd = blocks_capped(A.n, A.Pf.tpr, 2), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
-  k_residuals<<<nbd + nbe + nbc, QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
+int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
+  // thread-per-row ranges: enough blocks for 2 rows per thread, at most 16 resident-size waves
+  auto tgrid = [](int rows) { return std::max(1, std::min(148 * 16, (rows + 2 * QS_THREADS - 1) / (2 * QS_THREADS))); };
+  int launches = 0;
+  if (A.p > 0) {  // rows of A are the long ones when A is a design matrix: start them first
+    const int t = A.Ar.tpr;
+    if (t == 1) k_resid_eq<MODE_THREAD><<<tgrid(A.p), QS_THREADS, 0, st>>>(A);
+    else if (t == QS_TPR_CTA) k_resid_eq<MODE_CTA><<<blocks_for(A.p, t), QS_THREADS, 0, st>>>(A);
+    else k_resid_eq<MODE_GROUP><<<blocks_capped(A.p, t), QS_THREADS, 0, st>>>(A);
+    ++launches;
+  }
+  if (A.Pf.tpr == 1) k_resid_dual<MODE_THREAD><<<tgrid(A.n), QS_THREADS, 0, st>>>(A);
+  else k_resid_dual<MODE_GROUP><<<blocks_capped(A.n, A.Pf.tpr, 2), QS_THREADS, 0, st>>>(A);
+  {
+    const int t = A.Gr.tpr;
+    if (t == 1) k_resid_cone<MODE_THREAD><<<tgrid(A.m), QS_THREADS, 0, st>>>(A);
+    else if (t == QS_TPR_CTA) k_resid_cone<MODE_CTA><<<blocks_for(A.m, t), QS_THREADS, 0, st>>>(A);
+    else k_resid_cone<MODE_GROUP><<<blocks_capped(A.m, t), QS_THREADS, 0, st>>>(A);
+  }
+  return launches + 2;
 }
 
 void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st) {

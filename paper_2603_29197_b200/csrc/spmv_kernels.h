@@ -35,7 +35,7 @@ struct KktResidualArgs {
 };
 
 int qsk_pick_tpr(i64 nnz, i64 rows);
-void qsk_residuals(const ResidualArgs& A, cudaStream_t st);
+int qsk_residuals(const ResidualArgs& A, cudaStream_t st);  // returns the number of kernels launched (2 or 3)
 void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st);
 void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cudaStream_t st);
 void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out,

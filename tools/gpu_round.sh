@@ -12,11 +12,14 @@ python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "
 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
 python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 python tests/gpu_microbench.py > $OUT/microbench.txt 2>&1
-# launch list of the bench command (resident arm only: 1 warm-up solve + 1 timed solve)
+# the torchrun launch the driver uses for N > 1, here with one rank (NCCL init, barrier, max over ranks)
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
+    bench.py --gpus 1 --steps 1 --warmup 1 --e2e-steps 1 --no-cpu > $OUT/bench_torchrun1.json 2> $OUT/bench_torchrun1.err
+# launch list of the bench command (resident arm only: setup + ONE solve; shares, not absolutes)
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 1 --warmup 1 --no-cpu --e2e-steps 0 > $OUT/bench_under_ncu.log 2>&1
+    python bench.py --steps 1 --warmup 0 --no-cpu --e2e-steps 0 > $OUT/bench_under_ncu.log 2>&1
 # full capture of the dominant hot-path kernel (and the other cone kernels) on the C4 cone layout
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_neg_wtw|cone_kernel|k_residuals' -c 16 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_neg_wtw|cone_kernel|k_resid|k_mu_aff|k_update_iterate' -c 24 \
     -o $OUT/hot_kernels -f python tests/gpu_microbench.py 10000 20 250 0 1 > $OUT/ncu_full.log 2>&1
 ls -la $OUT
 tail -3 $OUT/pytest_gpu.log; cat $OUT/bench.json | cut -c1-3000

@@ -27,7 +27,7 @@ dst = os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)
 
 for name in ("bench.json", "bench_reference.json", "microbench.txt", "pytest_gpu.log", "smoke.log", "gpu.txt",
-             "bench_scaling.txt", "coldbench.txt"):
+             "bench_torchrun1.json"):
     p = os.path.join(src, name)
     if os.path.exists(p) and os.path.getsize(p) > 0:
         shutil.copy(p, os.path.join(dst, f"{tag}_{name}"))
