@@ -257,11 +257,14 @@ def run_ours(args):
             res = e2e_once()
         barrier()
         e2e_s = (time.perf_counter() - te) / args.e2e_steps
-    # host -> device per e2e step: the row views of P/A/G (int32 index + fp64 value), c/b/h, and the assembled
-    # KKT system (int64 column pointers, int32 rows, fp64 values, int64 slot map); device -> host: x, y, z, s
+    # bytes per e2e step, counted by the library from the buffers it copies: host -> device = row views of P/A/G
+    # (int32 index + fp64 value), c/b/h, the KKT column pointers and the analysis structures (the KKT entries are
+    # written by the device); device -> host = the scalar block of every phase and x, y, z, s at the end
+    if args.e2e_steps > 0:
+        h2d, d2h = res.timers["h2d_bytes"], res.timers["d2h_bytes"]
+    else:
+        h2d = d2h = 0
     knnz = configs.kkt_nnz(data)
-    h2d = 12 * 2 * (data.P.nnz + data.A.nnz + data.G.nnz) + 8 * (n + p + m) + 8 * (n + p + m + 1) + 12 * knnz + 8 * S
-    d2h = 8 * (n + p + 2 * m)
 
     if world > 1:
         t = torch.tensor([per_solve, e2e_s], dtype=torch.float64, device="cuda")

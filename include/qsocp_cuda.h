@@ -163,6 +163,9 @@ int qs_set_scaling(qs_handle* h, const double* w, const double* eta, const doubl
  * timers = {cone, kkt_update, residual, factor, solve, refine_spmv, analysis, h2d}; launches of own kernels so far */
 int qs_get_counters(qs_handle* h, int64_t* n_factor, int64_t* n_solve, int64_t* n_launches);
 int qs_get_timers(qs_handle* h, double* timers8);
+/* bytes copied host -> device (problem data, KKT column pointers, analysis structures) and device -> host (scalar
+ * blocks per phase, the final iterate) by this handle so far */
+int qs_get_transfer_bytes(qs_handle* h, int64_t* h2d, int64_t* d2h);
 int qs_get_factor_stats(qs_handle* h, double* stats8);
 /* time `reps` launches of one hot-path kernel on the current state (CUDA events on the handle's stream);
  * kernel ids in INTEGRATION.md.  Returns mean milliseconds per launch. */

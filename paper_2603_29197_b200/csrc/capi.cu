@@ -23,6 +23,7 @@ enum TimerCat { T_CONE = 0, T_KKT, T_RESID, T_FACTOR, T_SOLVE, T_REFINE, T_ANALY
 struct DevPool {
   std::vector<void*> ptrs;
   size_t bytes = 0;
+  size_t uploaded = 0;  // host -> device bytes copied through this pool
   template <class T>
   T* alloc(size_t count) {
     void* p = nullptr;
@@ -39,6 +40,7 @@ struct DevPool {
   T* upload(const T* src, size_t count, cudaStream_t st) {
     T* d = alloc<T>(count);
     if (d && count) cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, st);
+    if (d) uploaded += count * sizeof(T);
     return d;
   }
   void release() {
@@ -129,6 +131,7 @@ struct qs_handle {
   double norm_c = 0, norm_b = 0, norm_h = 0;
   // KKT
   i64 knnz = 0;
+  i64 d2h_bytes = 0, h2d_extra = 0;  // transfer accounting (qs_get_transfer_bytes)
   std::vector<i64> Kp_h;  // host copy of the KKT column pointers (the entries live on the device only)
   i64* d_Kp = nullptr;
   int* d_Ki = nullptr;
@@ -183,6 +186,7 @@ bool ensure_scratch(qs_handle* h) {
 }
 
 int fetch_scalars(qs_handle* h) {
+  h->d2h_bytes += SC_COUNT * sizeof(double);
   CK(h, cudaMemcpyAsync(h->scalars_host, h->scalars, SC_COUNT * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   h->tm.collect();
@@ -956,6 +960,7 @@ int qs_linsys_update_identity(qs_handle* h) {
   CK(h, cudaMemcpyAsync(h->wbar, e.data(), h->m * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   for (int i = 0; i < h->L.l; ++i) e[i] = 1.0;
   CK(h, cudaMemcpyAsync(h->lam, e.data(), h->m * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  h->h2d_extra += (h->L.l + h->L.nsoc + 2 * h->m) * (i64)sizeof(double);
   int rc = scatter_scaling(h, h->w, h->eta, h->wbar);
   CK(h, cudaStreamSynchronize(h->stream));
   return rc;
@@ -1124,6 +1129,7 @@ int qs_get_iterate(qs_handle* h, double* x, double* y, double* z, double* s) {
     sz = t + h->n + h->p;
     ss = h->tmp_m;
   }
+  h->d2h_bytes += ((x ? h->n : 0) + (y ? h->p : 0) + (z ? h->m : 0) + (s ? h->m : 0)) * (i64)sizeof(double);
   if (x) CK(h, cudaMemcpyAsync(x, sx, h->n * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (y) CK(h, cudaMemcpyAsync(y, sy, h->p * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (z) CK(h, cudaMemcpyAsync(z, sz, h->m * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1181,6 +1187,13 @@ int qs_get_counters(qs_handle* h, int64_t* n_factor, int64_t* n_solve, int64_t* 
   if (n_factor) *n_factor = h->n_factor;
   if (n_solve) *n_solve = h->n_solve;
   if (n_launches) *n_launches = h->launches;
+  return QS_OK;
+}
+
+int qs_get_transfer_bytes(qs_handle* h, int64_t* h2d, int64_t* d2h) {
+  if (!h) return QS_E_INVALID;
+  if (h2d) *h2d = (int64_t)(h->cone_pool.uploaded + h->prob_pool.uploaded + h->ls.h2d_bytes) + h->h2d_extra;
+  if (d2h) *d2h = h->d2h_bytes;
   return QS_OK;
 }
 

@@ -102,10 +102,12 @@ struct LinSys {
   std::vector<i64> lvslot, eaptr;   // per level: slot range, extend-add item range
   std::vector<int> lv_tpr;          // per level: lanes per slot in the forward-solve gather
   bool use_lists = true;
+  bool use_cluster = true;  // cluster-of-CTAs triangular solves for levels with at most 16 large fronts
   std::vector<void*> owned;
   double dyn_eps = 1e-14;
   double analysis_seconds = 0.0;
   size_t device_bytes = 0;
+  size_t h2d_bytes = 0;  // host -> device bytes copied by analyze()
 
   // Kp/Ki: host pattern (upper CSC) -- the full matrix or its compact form without the off-diagonal entries of
   // the clique blocks; knnz_full / d_Kp / d_Ki: the full matrix on the device.

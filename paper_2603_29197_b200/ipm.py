@@ -163,6 +163,12 @@ class DeviceSolver:
         self.lib.qs_get_counters(self.h, C.byref(f), C.byref(s), C.byref(k))
         return f.value, s.value, k.value
 
+    def transfer_bytes(self):
+        """(host -> device, device -> host) bytes this handle has copied so far."""
+        a, b = C.c_int64(), C.c_int64()
+        self.lib.qs_get_transfer_bytes(self.h, C.byref(a), C.byref(b))
+        return a.value, b.value
+
     def timers(self) -> dict:
         t = np.zeros(8)
         self.lib.qs_get_timers(self.h, _lib.ptr(t))
@@ -254,6 +260,7 @@ def solve(data: ProblemData, settings: Settings | None = None, backend_name: str
         n_factor, n_solve, launches = dev.counters()
         timers = dev.timers()
         timers["gpu_launches"] = launches
+        timers["h2d_bytes"], timers["d2h_bytes"] = dev.transfer_bytes()
         timers.update({f"factor_{k}": v for k, v in dev.factor_stats().items()})
         return SolveResult(status=status, x=it.x, y=it.y, z=it.z, s=it.s, objective=_objective(data, it.x),
                            iterations=iterations, setup_seconds=t1 - t0, solve_seconds=solve_seconds,
