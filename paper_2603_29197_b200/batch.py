@@ -38,20 +38,34 @@ def _default_solve(data, settings):
     return solve(data, settings)
 
 
-def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: int = 1, solve_fn=None, group=None):
+def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: int = 1, solve_fn=None, group=None,
+                workers: int = 1):
     """Solve instances {i : i mod world == rank}; gather records on rank 0.
 
     make_instance(i) -> ProblemData.  solve_fn(data, settings) -> SolveResult
-    (defaults to the CUDA path on settings.device).  Returns
+    (defaults to the CUDA path on settings.device).  workers > 1 keeps that many instances in flight on this rank's
+    GPU, each on its own handle and CUDA stream (a handle is single-threaded, distinct handles are independent;
+    ctypes releases the GIL inside the library): small instances are bound by kernel latency, not by the SMs, so
+    their kernels overlap -- the reference's analogue is the thread pool of its bench runner
+    (pkg/src/qsocp/bench/runner.py:107-117).  Returns
     (records sorted by index on rank 0 / this rank's records elsewhere, wall seconds of this rank).
     """
     solve_fn = solve_fn or _default_solve
-    mine = []
-    t0 = time.perf_counter()
-    for i in shard(count, rank, world):
+
+    def one(i):
         res = solve_fn(make_instance(i), settings)
-        mine.append(InstanceRecord(i, rank, getattr(res.status, "value", str(res.status)), int(res.iterations),
-                                   float(res.objective), float(res.setup_seconds), float(res.solve_seconds)))
+        return InstanceRecord(i, rank, getattr(res.status, "value", str(res.status)), int(res.iterations),
+                              float(res.objective), float(res.setup_seconds), float(res.solve_seconds))
+
+    t0 = time.perf_counter()
+    todo = shard(count, rank, world)
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            mine = list(pool.map(one, todo))
+    else:
+        mine = [one(i) for i in todo]
     wall = time.perf_counter() - t0
     if world == 1:
         return mine, wall

@@ -1004,6 +1004,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   if (!d_leaf || !d_gen || !d_small || !d_blk || !d_slabs) return "cudaMalloc failed for LDL work lists";
   // ---- assembly lists (AsmLists): slots of the fronts that have children, level by level
   use_cluster = getenv("QS_LDL_LOCKSTEP") == nullptr;
+  use_graphs = getenv("QS_NO_GRAPH") == nullptr;
   use_lists = getenv("QS_LDL_SEARCH") == nullptr && S.Boff[S.nsup] < ((i64)1 << 31);
   if (use_lists) {
     std::vector<i64> slot_base(S.nsup, -1);
@@ -1144,7 +1145,51 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   return std::string();
 }
 
+namespace {
+// Replay the launches of `body` from a graph captured on first use for the argument pair (a, b).
+template <class Body>
+void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const void* a, const void* b, cudaStream_t st,
+                 Body body) {
+  if (!enabled) {
+    body();
+    return;
+  }
+  for (const LinSys::GraphEntry& e : cache)
+    if (e.a == a && e.b == b) {
+      cudaGraphLaunch(e.exec, st);
+      return;
+    }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone || cache.size() >= 16 ||
+      cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    body();  // already inside someone else's capture, too many variants, or capture unavailable
+    return;
+  }
+  body();
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  if (cudaStreamEndCapture(st, &g) == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+    cache.push_back(LinSys::GraphEntry{a, b, exec});
+    cudaGraphLaunch(exec, st);
+  } else {
+    cudaGetLastError();
+    body();
+  }
+  if (g) cudaGraphDestroy(g);
+}
+}  // namespace
+
 void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
+  run_graphed(factor_graphs, use_graphs, d_Kx, scalars, st, [&]() { factor_launches(d_Kx, scalars, st); });
+}
+
+void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
+  run_graphed(solve_graphs, use_graphs, d_rhs, d_sol, st, [&]() { solve_launches(d_rhs, d_sol, st); });
+}
+
+void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t st) {
   cudaMemsetAsync(L, 0, S.Loff[S.nsup] * 8, st);
   if (S.Uoff[S.nsup] > 0) cudaMemsetAsync(U, 0, S.Uoff[S.nsup] * 8, st);
   k_scatter_values<<<grid_for(knnz), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
@@ -1203,7 +1248,7 @@ void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
   }
 }
 
-void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
+void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st) {
   k_permute_in<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, d_rhs, xw);
   const unsigned leaf_grid = (unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS);
   if (n_leaf > 0) k_leaf_fwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw, B);
@@ -1297,6 +1342,10 @@ int LinSys::launches_per_solve() const {
 }
 
 void LinSys::release() {
+  for (GraphEntry& e : factor_graphs) cudaGraphExecDestroy(e.exec);
+  for (GraphEntry& e : solve_graphs) cudaGraphExecDestroy(e.exec);
+  factor_graphs.clear();
+  solve_graphs.clear();
   for (void* p : owned) cudaFree(p);
   owned.clear();
   L = U = Dg = B = xw = reg = nullptr;

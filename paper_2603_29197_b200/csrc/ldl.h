@@ -114,8 +114,20 @@ struct LinSys {
   std::string analyze(i64 N, const i64* Kp, const i64* Ki, i64 knnz_full, const i64* d_Kp, const int* d_Ki, int order,
                       const i64* user_perm, i64 ncliques, const i64* clique_start, const i64* clique_size, i64 n_pos,
                       double static_reg, cudaStream_t st);
+  // The launch sequences of factor() and solve() depend only on the analysis, so each is captured once into a CUDA
+  // graph (per distinct argument tuple) and replayed: a small problem (MPC instance, 10^3 launches of a few
+  // microseconds each) is otherwise bound by launch overhead.  QS_NO_GRAPH=1 launches directly.
   void factor(const double* d_Kx, double* scalars, cudaStream_t st);
   void solve(const double* d_rhs, double* d_sol, cudaStream_t st);  // (L D L')^{-1} rhs, no refinement
+  void factor_launches(const double* d_Kx, double* scalars, cudaStream_t st);
+  void solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st);
+  struct GraphEntry {
+    const void* a;
+    const void* b;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> factor_graphs, solve_graphs;
+  bool use_graphs = true;
   int launches_per_factor() const;
   int launches_per_solve() const;
   void release();

@@ -27,7 +27,8 @@ dst = os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)
 
 for name in ("bench.json", "bench_reference.json", "microbench.txt", "pytest_gpu.log", "smoke.log", "gpu.txt",
-             "bench_torchrun1.json"):
+             "bench_torchrun1.json", "bench_C1_random_qp.json", "bench_C2_lasso.json", "bench_C3_portfolio.json",
+             "bench_C5_mpc.json", "c5_batch_throughput.txt", "ldl_factor_solve_ms.txt"):
     p = os.path.join(src, name)
     if os.path.exists(p) and os.path.getsize(p) > 0:
         shutil.copy(p, os.path.join(dst, f"{tag}_{name}"))
