@@ -162,6 +162,12 @@ int qs_set_scaling(qs_handle* h, const double* w, const double* eta, const doubl
 /* counters (linsys.py:30-31) and device timers in seconds:
  * timers = {cone, kkt_update, residual, factor, solve, refine_spmv, analysis, h2d}; launches of own kernels so far */
 int qs_get_counters(qs_handle* h, int64_t* n_factor, int64_t* n_solve, int64_t* n_launches);
+/* Pattern reuse (no reference counterpart -- SPEC.md lists parametric updates as a non-goal): new
+ * VALUES for P (upper CSC order), A, G (CSC order) and/or c, b, h with the sparsity pattern given to qs_setup.  Null =
+ * unchanged.  Ordering, symbolic analysis, index maps and launch graphs are kept; the next solve starts from
+ * qs_initialize_iterate. */
+int qs_update_values(qs_handle* h, const double* Px, const double* Ax, const double* Gx, const double* c,
+                     const double* b, const double* hvec);
 int qs_get_timers(qs_handle* h, double* timers8);
 /* bytes copied host -> device (problem data, KKT column pointers, analysis structures) and device -> host (scalar
  * blocks per phase, the final iterate) by this handle so far */

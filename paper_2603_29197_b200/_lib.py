@@ -85,6 +85,7 @@ SIGNATURES = {
     "qs_get_counters": (C.c_int, [vp, i64p, i64p, i64p]),
     "qs_get_timers": (C.c_int, [vp, vp]),
     "qs_get_factor_stats": (C.c_int, [vp, vp]),
+    "qs_update_values": (C.c_int, [vp] * 7),
     "qs_get_transfer_bytes": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "qs_time_kernel": (C.c_int, [vp, C.c_int, C.c_int, f64p]),
     "qs_time_kernel_cold": (C.c_int, [vp, C.c_int, C.c_int, f64p]),

@@ -38,6 +38,37 @@ def _default_solve(data, settings):
     return solve(data, settings)
 
 
+def pattern_reuse_solver():
+    """solve_fn for batches whose instances share one sparsity pattern (MPC trajectories, parametric sweeps): every
+    worker thread keeps ONE device handle; the first instance pays setup + analysis, the following ones only upload
+    their numbers (Solver.update -> qs_update_values)."""
+    import threading
+
+    import numpy as np
+
+    from .api import Solver
+
+    tls = threading.local()
+
+    def same_pattern(a, b):
+        return (a.n, a.m, a.p) == (b.n, b.m, b.p) and a.cone == b.cone and all(
+            np.array_equal(getattr(a, k).col_pointers, getattr(b, k).col_pointers)
+            and np.array_equal(getattr(a, k).row_indices, getattr(b, k).row_indices) for k in "PAG")
+
+    def solve_fn(d, settings):
+        s = getattr(tls, "solver", None)
+        if s is not None and tls.settings is settings and same_pattern(s._data, d):
+            s.update(P=d.P, c=d.c, A=d.A, b=d.b, G=d.G, h=d.h)
+        else:
+            kw = {} if settings is None else dict(vars(settings))
+            s = Solver("cuda").setup(d.n, d.m, d.p, d.P, d.c, d.A, d.b, d.G, d.h, d.cone.orthant_dim,
+                                     len(d.cone.soc_dims), d.cone.soc_dims, **kw)
+            tls.solver, tls.settings = s, settings
+        return s.solve()
+
+    return solve_fn
+
+
 def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: int = 1, solve_fn=None, group=None,
                 workers: int = 1):
     """Solve instances {i : i mod world == rank}; gather records on rank 0.

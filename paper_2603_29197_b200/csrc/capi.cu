@@ -126,11 +126,14 @@ struct qs_handle {
   bool have_problem = false;
   i64 n = 0, p = 0, m = 0, N = 0;
   qs_settings st{};
-  Csr Pf{}, At{}, Gt{}, Ar{}, Gr{};
+  Csr Pf{}, At{}, Gt{}, Ar{}, Gr{}, Pu{};
+  // value maps for qs_update_values: Ar.val[k] = Ax[ar_map[k]], Gr.val[k] = Gx[gr_map[k]], Pf.val[k] = Px[pf_map[k]]
+  int *ar_map = nullptr, *gr_map = nullptr, *pf_map = nullptr;
   double *c = nullptr, *b = nullptr, *hv = nullptr;
   double norm_c = 0, norm_b = 0, norm_h = 0;
   // KKT
   i64 knnz = 0;
+  i64 nnzP = 0, nnzPf = 0, nnzA = 0, nnzG = 0;
   i64 d2h_bytes = 0, h2d_extra = 0;  // transfer accounting (qs_get_transfer_bytes)
   std::vector<i64> Kp_h;  // host copy of the KKT column pointers (the entries live on the device only)
   i64* d_Kp = nullptr;
@@ -746,22 +749,40 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   for (i64 r = 0; r < n; ++r) Pfp[r + 1] += Pfp[r];
   std::vector<i64> Pfi(Pfp[n]);
   std::vector<double> Pfx(Pfp[n]);
+  std::vector<int> pf_map(Pfp[n]);
   {
     std::vector<i64> next(Pfp.begin(), Pfp.end() - 1);
     for (i64 j = 0; j < n; ++j) {
       for (i64 k = Pp[j]; k < Pp[j + 1]; ++k) {  // row j receives its cols i < j (and the diagonal)
         const i64 i = Pi[k];
         Pfi[next[j]] = i;
+        pf_map[next[j]] = (int)k;
         Pfx[next[j]++] = Px[k];
       }
       for (i64 k = Pp[j]; k < Pp[j + 1]; ++k) {  // rows i < j receive col j
         const i64 i = Pi[k];
         if (i == j) continue;
         Pfi[next[i]] = j;
+        pf_map[next[i]] = (int)k;
         Pfx[next[i]++] = Px[k];
       }
     }
   }
+  // where every entry of the row views of A and G comes from (for value-only updates): transpose the index vector
+  std::vector<int> ar_map(nnzA), gr_map(nnzG);
+  {
+    std::vector<double> iota(std::max(nnzA, nnzG)), tmp(std::max(nnzA, nnzG));
+    for (size_t k = 0; k < iota.size(); ++k) iota[k] = (double)k;
+    std::vector<i64> tp(std::max(p, m) + 1), ti(std::max(nnzA, nnzG));
+    hs_transpose(p, n, (const i64*)Ap, (const i64*)Ai, iota.data(), tp.data(), ti.data(), tmp.data());
+    for (i64 k = 0; k < nnzA; ++k) ar_map[k] = (int)tmp[k];
+    hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, iota.data(), tp.data(), ti.data(), tmp.data());
+    for (i64 k = 0; k < nnzG; ++k) gr_map[k] = (int)tmp[k];
+  }
+  h->nnzP = nnzP;
+  h->nnzPf = Pfp[n];
+  h->nnzA = nnzA;
+  h->nnzG = nnzG;
   // ---- KKT system: column pointers + compact pattern on the host (O(N + nnz(P,A,G))); the 10^8 entries
   // themselves (row indices, initial values, slot -> position map) are written by the device (qsk_kkt_fill).
   // QS_HOST_ASSEMBLY=1 keeps the original host assembly + upload as the checked alternative.
@@ -810,9 +831,13 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
     h->d_pos = h->prob_pool.upload(pos_full.data(), pos_full.size(), st);
     CK(h, cudaStreamSynchronize(st));
   } else {
-    Csr Pu{};
+    Csr& Pu = h->Pu;
     if (!make_csr(h, &Pu, n, n, (const i64*)Pp, (const i64*)Pi, Px))  // CSC of upper(P) = CSR of its transpose
       return fail(h, QS_E_MEMORY, "out of device memory for P");
+    h->ar_map = h->prob_pool.upload(ar_map.data(), ar_map.size(), st);
+    h->gr_map = h->prob_pool.upload(gr_map.data(), gr_map.size(), st);
+    h->pf_map = h->prob_pool.upload(pf_map.data(), pf_map.size(), st);
+    if (!h->ar_map || !h->gr_map || !h->pf_map) return fail(h, QS_E_MEMORY, "out of device memory for the value maps");
     h->d_Ki = h->prob_pool.alloc<int>(h->knnz);
     h->d_Kx = h->prob_pool.alloc<double>(h->knnz);
     h->d_pos = h->prob_pool.alloc<i64>(h->S);
@@ -922,6 +947,59 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
 #define NEED_PROBLEM(h)                                                                                     \
   if (!(h) || !(h)->have_problem) return (h) ? fail(h, QS_E_INVALID, "qs_setup first") : QS_E_INVALID;       \
   cudaSetDevice((h)->device);
+
+// Same sparsity pattern, new numbers (parametric re-solve).  Any pointer may be null (= unchanged).
+// Keeps the row views' structure, the KKT pattern, the ordering, the symbolic analysis, the assembly lists and the
+// captured launch graphs; re-uploads the values (host -> device: exactly the arrays given), regathers the row
+// views on the device and rewrites the KKT values.  The next qs_initialize_iterate starts a fresh solve.
+int qs_update_values(qs_handle* h, const double* Px, const double* Ax, const double* Gx, const double* c,
+                     const double* b, const double* hvec) {
+  NEED_PROBLEM(h)
+  if (h->rD) return fail(h, QS_E_INVALID, "qs_update_values with ruiz_iters > 0 is not supported");
+  if (!h->pf_map) return fail(h, QS_E_INVALID, "qs_update_values needs the device-assembled KKT path");
+  cudaStream_t st = h->stream;
+  const i64 n = h->n, p = h->p, m = h->m;
+  auto up = [&](const double* src, const double* dst, i64 count) {
+    if (count > 0) cudaMemcpyAsync(const_cast<double*>(dst), src, count * sizeof(double), cudaMemcpyHostToDevice, st);
+    h->h2d_extra += count * (i64)sizeof(double);
+  };
+  if (Px) {
+    i64 nnzP = 0, nnzPf = 0;
+    nnzP = h->nnzP;
+    nnzPf = h->nnzPf;
+    up(Px, h->Pu.val, nnzP);
+    qsk_gather(nnzPf, h->Pu.val, h->pf_map, const_cast<double*>(h->Pf.val), st);
+  }
+  if (Ax) {
+    up(Ax, h->At.val, h->nnzA);
+    qsk_gather(h->nnzA, h->At.val, h->ar_map, const_cast<double*>(h->Ar.val), st);
+  }
+  if (Gx) {
+    up(Gx, h->Gt.val, h->nnzG);
+    qsk_gather(h->nnzG, h->Gt.val, h->gr_map, const_cast<double*>(h->Gr.val), st);
+  }
+  if (c) {
+    up(c, h->c, n);
+    h->norm_c = inf_norm(c, n);
+  }
+  if (b) {
+    up(b, h->b, p);
+    h->norm_b = inf_norm(b, p);
+  }
+  if (hvec) {
+    up(hvec, h->hv, m);
+    h->norm_h = inf_norm(hvec, m);
+  }
+  if (Px || Ax || Gx) {
+    WtwPlan plan = h->wp;
+    plan.slot_start = h->d_slot_start;
+    qsk_kkt_fill(plan, (int)n, (int)p, h->Pu, h->Ar, h->Gr, h->d_Kp, h->d_Ki, h->d_Kx, h->d_pos, st);
+    h->launches += 4;
+  }
+  h->factored = false;
+  CK(h, cudaStreamSynchronize(st));  // the caller's buffers may be released on return
+  return check_launch(h, "update_values");
+}
 
 int64_t qs_kkt_size(qs_handle* h, int64_t* nnz, int64_t* slots) {
   if (!h || !h->have_problem) return -1;

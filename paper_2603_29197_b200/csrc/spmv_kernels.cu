@@ -520,6 +520,11 @@ __global__ void __launch_bounds__(QS_THREADS) k_axpby(i64 n, double a, const dou
     out[i] = a * x[i] + (y ? b * y[i] : 0.0);
 }
 
+__global__ void __launch_bounds__(QS_THREADS) k_gather(i64 n, const double* __restrict__ src,
+                                                       const int* __restrict__ map, double* __restrict__ dst) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) dst[i] = src[map[i]];
+}
+
 __global__ void __launch_bounds__(QS_THREADS) k_absmax(i64 n, const double* x, double* out, double* nonfinite,
                                                        GridRed gr) {
   double v[1] = {0.0};
@@ -604,6 +609,11 @@ void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const doubl
   if (ncols <= 0) return;
   const i64 blocks = ((i64)ncols * 32 + QS_THREADS - 1) / QS_THREADS;
   k_spmv_sym_upper_csc<<<(unsigned)blocks, QS_THREADS, 0, st>>>(ncols, cp, ri, vx, x, out);
+}
+
+void qsk_gather(i64 n, const double* src, const int* map, double* dst, cudaStream_t st) {
+  if (n <= 0) return;
+  k_gather<<<vgrid(n), QS_THREADS, 0, st>>>(n, src, map, dst);
 }
 
 void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st) {

@@ -40,5 +40,6 @@ void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st);
 void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cudaStream_t st);
 void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out,
                             cudaStream_t st);
+void qsk_gather(i64 n, const double* src, const int* map, double* dst, cudaStream_t st);  // dst[i] = src[map[i]]
 void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st);
 void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st);

@@ -99,6 +99,42 @@ class DeviceSolver:
     def _check(self, rc, what=""):
         _lib.check(self.lib, self.h, rc, what)
 
+    def update_values(self, P=None, A=None, G=None, c=None, b=None, h=None):
+        """New numbers on the SAME sparsity pattern (qs_update_values): keeps the KKT pattern, ordering, symbolic
+        analysis, index maps and launch graphs of this handle.  Matrices are SparseMatrixCSC with exactly the pattern
+        given at setup (BadSparseStructure otherwise); vectors must keep their length.  The next run() is a fresh
+        solve of the updated problem."""
+        import dataclasses
+
+        from .errors import BadSparseStructure, DimensionMismatch
+
+        d = self.data
+        new = {}
+        vals = []
+        for name, M in (("P", P), ("A", A), ("G", G)):
+            if M is None:
+                vals.append(None)
+                continue
+            old = getattr(d, name)
+            if (M.rows, M.cols) != (old.rows, old.cols) or not np.array_equal(M.col_pointers, old.col_pointers) \
+                    or not np.array_equal(M.row_indices, old.row_indices):
+                raise BadSparseStructure(f"update_values: {name} must keep the sparsity pattern given at setup")
+            vals.append(_lib.f64(M.values))
+            new[name] = M
+        for name, v in (("c", c), ("b", b), ("h", h)):
+            if v is None:
+                vals.append(None)
+                continue
+            v = _lib.f64(v)
+            if v.shape != getattr(d, name).shape:
+                raise DimensionMismatch(f"update_values: {name} must keep its length")
+            if not np.all(np.isfinite(v)):
+                pass  # non-finite data surfaces as NUMERICAL_ERROR from the solve, as in the reference (ipm.py:96-102)
+            vals.append(v)
+            new[name] = v
+        self._check(self.lib.qs_update_values(self.h, *[_lib.ptr(v) for v in vals]), "update_values")
+        self.data = dataclasses.replace(d, **new)
+
     def set_stream(self, cuda_stream: int):
         """Run on an existing CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
         self._check(self.lib.qs_set_stream(self.h, C.c_void_p(cuda_stream)))
@@ -254,16 +290,23 @@ def solve(data: ProblemData, settings: Settings | None = None, backend_name: str
     validate_problem(data)
     dev = DeviceSolver(data, settings, ordering=ordering, user_perm=user_perm)
     try:
-        t1 = time.perf_counter()
-        status, iterations, it = dev.run(t0, iterate_hook)
-        solve_seconds = time.perf_counter() - t1
-        n_factor, n_solve, launches = dev.counters()
-        timers = dev.timers()
-        timers["gpu_launches"] = launches
-        timers["h2d_bytes"], timers["d2h_bytes"] = dev.transfer_bytes()
-        timers.update({f"factor_{k}": v for k, v in dev.factor_stats().items()})
-        return SolveResult(status=status, x=it.x, y=it.y, z=it.z, s=it.s, objective=_objective(data, it.x),
-                           iterations=iterations, setup_seconds=t1 - t0, solve_seconds=solve_seconds,
-                           factor_count=n_factor, solve_count=n_solve, timers=timers)
+        return solve_on(dev, t0, iterate_hook)
     finally:
         dev.close()
+
+
+def solve_on(dev: "DeviceSolver", t0: float, iterate_hook=None) -> SolveResult:
+    """One solve on an existing handle (fresh from setup or after update_values); counters and byte counts in the
+    result are those of THIS solve."""
+    f0, s0, l0 = dev.counters()
+    t1 = time.perf_counter()
+    status, iterations, it = dev.run(t0, iterate_hook)
+    solve_seconds = time.perf_counter() - t1
+    n_factor, n_solve, launches = dev.counters()
+    timers = dev.timers()
+    timers["gpu_launches"] = launches - (l0 if f0 else 0)  # the first solve also owns the setup launches
+    timers["h2d_bytes"], timers["d2h_bytes"] = dev.transfer_bytes()
+    timers.update({f"factor_{k}": v for k, v in dev.factor_stats().items()})
+    return SolveResult(status=status, x=it.x, y=it.y, z=it.z, s=it.s, objective=_objective(dev.data, it.x),
+                       iterations=iterations, setup_seconds=t1 - t0, solve_seconds=solve_seconds,
+                       factor_count=n_factor - f0, solve_count=n_solve - s0, timers=timers)

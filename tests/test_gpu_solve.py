@@ -222,3 +222,52 @@ def test_solve_with_long_design_rows_matches_oracle(oracle):
     assert res.status.value == ref.status == "Solved"
     assert abs(res.iterations - ref.iterations) <= 1
     assert abs(res.objective - ref.objective) <= 1e-6 * max(1.0, abs(ref.objective))
+
+
+def test_update_values_reuses_the_pattern_and_matches_a_fresh_solve():
+    """Solver.update (qs_update_values): same pattern, new numbers; the re-solve on the kept handle is bitwise the
+    solve of a fresh handle on the same numbers, and a different pattern is refused."""
+    import dataclasses
+
+    from paper_2603_29197_b200.errors import BadSparseStructure
+    from paper_2603_29197_b200.sparse import SparseMatrixCSC
+
+    d = problem_from_golden(load_golden("portfolio_4"))
+    s = qs.Solver("cuda").setup(d.n, d.m, d.p, d.P, d.c, d.A, d.b, d.G, d.h, d.cone.orthant_dim,
+                                len(d.cone.soc_dims), d.cone.soc_dims)
+    first = s.solve()
+    assert first.status is SolveStatus.SOLVED
+
+    def scaled(M, f):
+        return SparseMatrixCSC(M.rows, M.cols, M.col_pointers, M.row_indices, M.values * f)
+
+    d2 = dataclasses.replace(d, P=scaled(d.P, 1.5), c=d.c * 0.9, h=d.h + 0.05 * np.abs(d.h), G=scaled(d.G, 1.0))
+    second = s.update(P=d2.P, c=d2.c, G=d2.G, h=d2.h).solve()
+    fresh = run(d2)
+    assert second.status is fresh.status is SolveStatus.SOLVED
+    assert second.iterations == fresh.iterations and second.objective == fresh.objective
+    for k in "xyzs":
+        assert np.array_equal(getattr(second, k), getattr(fresh, k)), k
+    assert second.factor_count == second.iterations + 1 and second.solve_count == 2 * second.iterations + 2
+    # back to the original numbers: the original solution, bit for bit
+    third = s.update(P=d.P, c=d.c, G=d.G, h=d.h).solve()
+    for k in "xyzs":
+        assert np.array_equal(getattr(third, k), getattr(first, k)), k
+    # a different pattern is not an update
+    bad = SparseMatrixCSC(d.G.rows, d.G.cols, d.G.col_pointers, d.G.row_indices[::-1].copy(), d.G.values)
+    if not np.array_equal(bad.row_indices, d.G.row_indices):
+        with pytest.raises(BadSparseStructure):
+            s.update(G=bad)
+    s.close()
+
+
+def test_batch_with_pattern_reuse_matches_independent_solves():
+    from paper_2603_29197_b200 import configs
+    from paper_2603_29197_b200.batch import pattern_reuse_solver, solve_batch
+
+    probs = [configs.mpc(horizon=10, nx=6, nu=2, seed=i) for i in range(6)]
+    a, _ = solve_batch(lambda i: probs[i], len(probs), Settings())
+    b, _ = solve_batch(lambda i: probs[i], len(probs), Settings(), solve_fn=pattern_reuse_solver(), workers=2)
+    for ra, rb in zip(a, b):
+        assert ra.index == rb.index and ra.status == rb.status == "Solved"
+        assert ra.iterations == rb.iterations and ra.objective == rb.objective
