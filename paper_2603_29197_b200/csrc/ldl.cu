@@ -744,41 +744,34 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const double* Lp = L + S.Loff[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gt = rank * LDL_THREADS + tid, gstride = QS_CL * LDL_THREADS;
-  __shared__ double red[LDL_THREADS / 32][NB];
-  __shared__ double part[NB];  // this CTA's partial sums, read by rank 0 through distributed shared memory
+  __shared__ double part[LDL_THREADS / 32];  // this CTA's partial sums (one per warp), read by rank 0 through DSMEM
   const int last_kb = ((ns - 1) / NB) * NB;
+  // Column-oriented products: the 8 x QS_CL = 64 warps of the cluster take the 32 columns of the block, two warps
+  // per column (even / odd 32-row groups); a lane strides down its column (contiguous in memory), so a step costs
+  // one 5-round shuffle reduction per warp instead of 32 of them.
+  const int gw = rank * (LDL_THREADS / 32) + warp;  // 0 .. 63
+  const int kcol = gw & (NB - 1), half = gw >> 5;
   for (int kb = last_kb; kb >= 0; kb -= NB) {
     const int nb = min(NB, ns - kb);
-    // t[k] = sum over the rows below the block of L(r, kb + k) x_r, this CTA's share of the rows
-    double acc[NB];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) acc[k] = 0.0;
-    for (int r = kb + nb + gt; r < nr; r += gstride) {
-      const double xr = (r < ns) ? xw[c0 + r] : xw[S.rowidx[rp + r]];
-      const double* Lr = Lp + r + (i64)kb * nr;
-#pragma unroll
-      for (int k = 0; k < NB; ++k)
-        if (k < nb) acc[k] += Lr[(i64)k * nr] * xr;
+    double acc = 0.0;
+    if (kcol < nb) {
+      const double* Lc = Lp + (i64)(kb + kcol) * nr;
+      for (int r = kb + nb + lane + 32 * half; r < nr; r += 64) {
+        const double xr = (r < ns) ? xw[c0 + r] : xw[S.rowidx[rp + r]];
+        acc += Lc[r] * xr;
+      }
     }
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      double v = acc[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[warp][k] = v;
-    }
-    __syncthreads();
-    if (tid < NB) {
-      double t = 0.0;
-      for (int w = 0; w < LDL_THREADS / 32; ++w) t += red[w][tid];
-      part[tid] = t;
-    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[warp] = acc;
     cluster.sync();  // all partials published
     if (rank == 0 && warp == 0) {
       double x = (lane < nb) ? xw[c0 + kb + lane] : 0.0;
-      for (int c = 0; c < QS_CL; ++c) {  // fixed order: deterministic
-        const double* remote = cluster.map_shared_rank(part, c);
-        if (lane < nb) x -= remote[lane];
+      // column `lane` was summed by global warps `lane` (even row groups) and `lane + 32` (odd ones): fixed order
+      if (lane < nb) {
+        const double* r0p = cluster.map_shared_rank(part, lane >> 3);
+        const double* r1p = cluster.map_shared_rank(part, (lane >> 3) + 4);
+        x -= r0p[lane & 7] + r1p[lane & 7];
       }
       double lcol[NB];  // column kb + lane of the block below its diagonal, fetched up front
 #pragma unroll

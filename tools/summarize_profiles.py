@@ -21,7 +21,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
-dominant = sys.argv[2] if len(sys.argv) > 2 else "k_neg_wtw"
+dominant = sys.argv[2] if len(sys.argv) > 2 else r"k_neg_wtw<2, 1>"
 src = os.path.join(ROOT, "gpurun_out", tag)
 dst = os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)
