@@ -128,24 +128,13 @@ __global__ void __launch_bounds__(QS_THREADS)
         const int g0 = g_ptr[col], ng = g_ptr[col + 1] - g0;
         for (int t = sl; t < ng; t += 16) dst[t - ng] = g_val[g0 + t];
       }
-      // 128-bit stores: a lane writes the aligned pair (i, i+1); an odd first element goes out alone.  (ncu: the
-      // 64-bit version spent 20 % of its stall samples on STG issue with the L1/TEX pipe at 76 %.)
-      const double ne2 = mne2[c];
-      const double head = (j == 0) ? mA0[c] * wc[0] + ne2 : mA0[c] * wc[0];
-      const int par = (int)((reinterpret_cast<uintptr_t>(dst) >> 3) & 1);
-      if (par && sl == 0) dst[0] = head;
-      for (int i = par + 2 * sl; i <= j; i += 32) {
-        double v0 = A * wc[i];
-        if (i == 0) v0 = head;
-        else if (i == j) v0 = v0 + ne2;
-        if (i + 1 <= j) {
-          double v1 = A * wc[i + 1];
-          if (i + 1 == j) v1 = v1 + ne2;
-          *reinterpret_cast<double2*>(dst + i) = make_double2(v0, v1);
-        } else {
-          dst[i] = v0;
-        }
-      }
+      // 64-bit stores, 16 lanes = one contiguous 128-byte run.  (A 128-bit variant -- aligned pairs, odd head
+      // peeled -- halves the store instructions but measured 217 vs 213 us: the stall is back-pressure from the
+      // memory system, not store issue.)
+      for (int i = sl; i <= j; i += 16) dst[i] = A * wc[i];
+      // the two special entries are rewritten by the lane that just wrote them
+      if (sl == 0) dst[0] = (j == 0) ? mA0[c] * wc[0] + mne2[c] : mA0[c] * wc[0];
+      if (j > 0 && sl == (j & 15)) dst[j] = A * wc[j] + mne2[c];
     }
   }
 }
