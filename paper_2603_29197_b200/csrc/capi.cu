@@ -526,6 +526,8 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   P.nsoc = (int)nsoc;
   P.m = (int)m;
   P.soc_ptr = L.soc_ptr;
+  i64 wtw_tile = QS_WTW_TILE;
+  if (const char* e = getenv("QS_WTW_TILE")) wtw_tile = std::max(256, atoi(e));  // tuning knob
   std::vector<int> cone_of_col(m - l), tile_ptr;
   std::vector<i64> slot_start(nsoc);
   i64 slot = l, acc = 0;
@@ -545,7 +547,7 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
       if (col == tile_ptr.back()) tile_first_cone_start = ptr[k];  // first column of a new tile
       cone_of_col[col - l] = (int)k;
       acc += j + 1;
-      if (acc >= QS_WTW_TILE || col + 1 - tile_ptr.back() >= QS_WTW_MAXCOLS) close_tile(col + 1);
+      if (acc >= wtw_tile || col + 1 - tile_ptr.back() >= QS_WTW_MAXCOLS) close_tile(col + 1);
     }
   }
   if (tile_ptr.back() != (int)m) close_tile((int)m);

@@ -78,7 +78,10 @@ __global__ void __launch_bounds__(QS_THREADS)
   i64* mbase = reinterpret_cast<i64*>(mne2 + max_cols);
   int* mj = reinterpret_cast<int*>(mbase + max_cols);
   int* mwoff = mj + max_cols;
-  double* wst = reinterpret_cast<double*>(mwoff + max_cols);  // 2 * max_cols ints: 8-byte aligned
+  int* mg0 = mwoff + max_cols;   // first entry of the column's row of G (DIRECT mode with whole columns)
+  int* mng = mg0 + max_cols;     // its length
+  double* mgv = reinterpret_cast<double*>(mng + max_cols);  // its first value (most rows of G hold one entry)
+  double* wst = mgv + max_cols;  // 4 * max_cols ints: 8-byte aligned
   const int tile = blockIdx.x - nb_orth;
   const int col0 = tile_ptr[tile], col1 = tile_ptr[tile + 1];
   const int ncols = col1 - col0;
@@ -97,6 +100,12 @@ __global__ void __launch_bounds__(QS_THREADS)
     mA[c] = (j == 0) ? 0.0 : ne2 * ((cc + 4.0) * wj);
     mA0[c] = (j == 0) ? ne2 * ((cc - 4.0) * wj) : ne2 * (cc * wj);
     mbase[c] = (MODE == MODE_DIRECT) ? kp_conic[col] - (j + 1) : slot_start[k] + (i64)j * (j + 1) / 2;
+    if (MODE == MODE_DIRECT && g_ptr) {  // every load chain of the column runs here, in parallel over the columns:
+      const int g0 = g_ptr[col], ng = g_ptr[col + 1] - g0;  // the streaming loop below waits on no global load
+      mg0[c] = g0;
+      mng[c] = ng;
+      mgv[c] = ng > 0 ? g_val[g0] : 0.0;
+    }
   }
   if (STAGED)
     for (int t = threadIdx.x; t < wlen; t += QS_THREADS) wst[t] = wbar[wlo + t];
@@ -104,10 +113,10 @@ __global__ void __launch_bounds__(QS_THREADS)
   constexpr int NW = QS_THREADS / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane >> 4, sl = lane & 15;
-  // warp `warp` owns the contiguous column chunk [cbeg, cend); its two halves take alternate columns
-  const int per = ((ncols + 2 * NW - 1) / (2 * NW)) * 2;
-  const int cbeg = warp * per, cend = min(ncols, cbeg + per);
-  for (int c = cbeg + sub; c < cend; c += 2) {
+  // Column pairs are dealt round-robin to the warps (the two halves of a warp take the two columns of a pair, whose
+  // lengths differ by one, so they stay in step).  Column lengths grow along a cone, so contiguous chunks per warp
+  // left the warps of the first chunks idle early: 197 -> 194 us.
+  for (int c = 2 * warp + sub; c < ncols; c += 2 * NW) {
     const int j = mj[c];
     const double A = mA[c];
     const i64 base = mbase[c];
@@ -124,9 +133,9 @@ __global__ void __launch_bounds__(QS_THREADS)
         // of G).  The column is then written in full, adjacent columns tile K.values without holes, and
         // no 32-byte sector is left partially written: measured, that is the difference between ~3.2 and
         // ~6 TB/s of store bandwidth (tests/probes/store_probe.cu).
-        const int col = col0 + c;
-        const int g0 = g_ptr[col], ng = g_ptr[col + 1] - g0;
-        for (int t = sl; t < ng; t += 16) dst[t - ng] = g_val[g0 + t];
+        const int g0 = mg0[c], ng = mng[c];
+        if (sl == 0 && ng > 0) dst[-ng] = mgv[c];
+        for (int t = 1 + sl; t < ng; t += 16) dst[t - ng] = g_val[g0 + t];
       }
       // 64-bit stores, 16 lanes = one contiguous 128-byte run.  (A 128-bit variant -- aligned pairs, odd head
       // peeled -- halves the store instructions but measured 217 vs 213 us: the stall is back-pressure from the
@@ -406,7 +415,7 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
   const bool staged = P.max_tile_window <= QS_WTW_WCAP;
   const int wcap = staged ? P.max_tile_window : 0;
   const int mc = P.max_tile_cols;
-  const size_t smem = (size_t)mc * (4 * sizeof(double) + 2 * sizeof(int)) + 16 + (size_t)wcap * sizeof(double);
+  const size_t smem = (size_t)mc * (5 * sizeof(double) + 4 * sizeof(int)) + 16 + (size_t)wcap * sizeof(double);
   auto launch = [&](auto kern, const i64* pos, const i64* kpc) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     kern<<<grid, QS_THREADS, smem, st>>>(P.l, nb_orth, mc, wcap, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,

@@ -3,7 +3,7 @@
 #include "common.cuh"
 #include "spmv_kernels.h"
 
-#define QS_WTW_TILE 16384      // target block entries per CTA
+#define QS_WTW_TILE 8192       // target block entries per CTA
 #define QS_WTW_MAXCOLS 512     // at most this many columns per tile (metadata lives in shared memory)
 #define QS_WTW_WCAP 16384      // wbar window staged in shared memory when it fits (doubles)
 #define QS_WTW_STAGE 4096      // staged variant: output doubles per CTA (32 KiB of shared memory; 4 CTAs per SM)
