@@ -49,7 +49,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     for f in CPP:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         if force or _stale(obj, [src] + hdrs):
-            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-c", src, "-o", obj])
+            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-pthread", "-c", src, "-o", obj])
 
     def run(cmd):
         if verbose:
@@ -62,7 +62,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(run, jobs))
     objs = [os.path.join(OBJ, f + ".o") for f in CU + CPP]
     if force or jobs or _stale(LIB, objs):
-        run([NVCC, "-shared", "-o", LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a"])
+        run([NVCC, "-shared", "-o", LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-pthread"])
     return LIB
 
 

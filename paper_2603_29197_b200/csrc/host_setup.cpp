@@ -2,6 +2,8 @@
 #include "host_setup.h"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -761,15 +763,22 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   Upper B;
   std::vector<int> parent, post;
   permuted_upper(N, Kp, Ki, cof, cliques, iperm, &B);
+  lap("permuted pattern");
   etree_of(N, B, &parent);
+  lap("etree");
   postorder_of(N, parent, &post);
+  lap("postorder");
   {
     std::vector<int> perm2(N);
     for (i64 k = 0; k < N; ++k) perm2[k] = perm[post[k]];
     perm.swap(perm2);
     for (i64 k = 0; k < N; ++k) iperm[perm[k]] = (int)k;
     permuted_upper(N, Kp, Ki, cof, cliques, iperm, &B);
-    etree_of(N, B, &parent);
+    // the elimination tree of a postordered relabelling is the relabelled tree: no second etree pass
+    std::vector<int> where(N), parent2(N);
+    for (i64 k = 0; k < N; ++k) where[post[k]] = (int)k;
+    for (i64 k = 0; k < N; ++k) parent2[k] = parent[post[k]] >= 0 ? where[parent[post[k]]] : -1;
+    parent.swap(parent2);
   }
   for (i64 j = 0; j < N; ++j)
     if (parent[j] != -1 && parent[j] <= j) return "internal: tree is not postordered";
@@ -899,22 +908,44 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
     S->max_nr = std::max<int>(S->max_nr, (int)nr);
     S->max_ns = std::max<int>(S->max_ns, (int)ns);
   }
+  lap("offsets + flop count");
   S->rel.resize(S->relptr[nsup]);
-  for (int s = 0; s < nsup; ++s) {
-    const int par = S->parent[s];
-    if (par < 0) continue;
-    const int ns = S->col0[s + 1] - S->col0[s];
-    const int* prow = S->rowidx.data() + S->rowptr[par];
-    const i64 pn = S->rowptr[par + 1] - S->rowptr[par];
-    i64 at = 0;
-    int* rel = S->rel.data() + S->relptr[s];
-    for (i64 k = S->rowptr[s] + ns; k < S->rowptr[s + 1]; ++k) {
-      const int r = S->rowidx[k];
-      while (at < pn && prow[at] < r) ++at;
-      if (at >= pn || prow[at] != r) return "internal: child row missing from the parent front";
-      *rel++ = (int)at;
+  {
+    // independent per supernode: split over host threads
+    std::atomic<bool> missing{false};
+    auto work = [&](int s_lo, int s_hi) {
+      for (int s = s_lo; s < s_hi; ++s) {
+        const int par = S->parent[s];
+        if (par < 0) continue;
+        const int ns = S->col0[s + 1] - S->col0[s];
+        const int* prow = S->rowidx.data() + S->rowptr[par];
+        const i64 pn = S->rowptr[par + 1] - S->rowptr[par];
+        i64 at = 0;
+        int* rel = S->rel.data() + S->relptr[s];
+        for (i64 k = S->rowptr[s] + ns; k < S->rowptr[s + 1]; ++k) {
+          const int r = S->rowidx[k];
+          // both lists ascend; a leaf with 4 rows under a 700-row front must not walk the front: binary search
+          at = std::lower_bound(prow + at, prow + pn, r) - prow;
+          if (at >= pn || prow[at] != r) {
+            missing = true;
+            return;
+          }
+          *rel++ = (int)at;
+        }
+      }
+    };
+    const int nthreads = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (nsup < 100000 || nthreads == 1) {
+      work(0, nsup);
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < nthreads; ++t)
+        pool.emplace_back(work, (int)((i64)nsup * t / nthreads), (int)((i64)nsup * (t + 1) / nthreads));
+      for (auto& th : pool) th.join();
     }
+    if (missing) return "internal: child row missing from the parent front";
   }
+  lap("relative indices");
   std::vector<int> level(nsup, 0);
   int maxlevel = 0;
   for (int s = 0; s < nsup; ++s) {
@@ -933,6 +964,6 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   }
   S->perm.swap(perm);
   S->iperm.swap(iperm);
-  lap("rel indices + levels");
+  lap("levels");
   return std::string();
 }

@@ -130,30 +130,67 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 // List-driven extend-add (see AsmLists): a warp owns (column slot, row band) of a front outright and walks the
 // slot's child entries in their fixed order -- deterministic, no atomics, no searching.
+// TPR lanes own one work item.  TPR = 32 (root: ~50 rows per child and band): the per-child metadata (six
+// dependent loads: child id -> offsets, sizes, band bounds) is fetched for 32 list entries at a time, one entry per
+// lane, so the chains run in parallel and the entries are then processed from registers via shuffles.  TPR = 4
+// (children with a handful of update rows, e.g. the 1.35 M one-column leaves of C4): eight items per warp.
+template <int TPR>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_extend_add_list(DevSym S, AsmLists A, const EaItem* items, i64 nitems, double* L, double* U) {
-  const i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nitems) return;
-  const EaItem it = items[w];
+  const i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / TPR;
+  const int lane = threadIdx.x & (TPR - 1);
+  if (TPR == 32 ? w >= nitems : false) return;
+  const bool on = w < nitems;
+  const EaItem it = on ? items[w] : EaItem{0, -1};
   const int s = A.slot_front[it.slot], pc = A.slot_row[it.slot];
   const Front f = front_of(S, s, L, U);
   const i64 nr = f.nr, nu = f.nu;
   double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;  // indexed by parent row
-  const i64 e0 = A.gptr[it.slot], e1 = A.gptr[it.slot + 1];
-  for (i64 e = e0; e < e1; ++e) {
-    const int c = A.gchild[e];
-    const int cc = A.gsrc[e] - (int)S.Boff[c];
-    const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - (S.col0[c + 1] - S.col0[c]);
-    int r_lo = cc, r_hi = nuc;
-    if (it.band >= 0) {
-      const int* bs = A.bandstart + A.bandptr[c];
-      r_lo = max(cc, bs[it.band]);
-      r_hi = bs[it.band + 1];
+  const i64 e0 = on ? A.gptr[it.slot] : 0, e1 = on ? A.gptr[it.slot + 1] : 0;
+  if (TPR == 32) {
+    for (i64 eb = e0; eb < e1; eb += 32) {
+      // lane i: metadata of entry eb + i
+      const i64 e = eb + lane;
+      i64 uoff = 0, roff = 0;
+      int r_lo = 0, r_hi = 0;
+      if (e < e1) {
+        const int c = A.gchild[e];
+        const int cc = A.gsrc[e] - (int)S.Boff[c];
+        const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - (S.col0[c + 1] - S.col0[c]);
+        r_lo = cc;
+        r_hi = nuc;
+        if (it.band >= 0) {
+          const int* bs = A.bandstart + A.bandptr[c];
+          r_lo = max(cc, bs[it.band]);
+          r_hi = bs[it.band + 1];
+        }
+        uoff = S.Uoff[c] + (i64)cc * nuc;
+        roff = S.relptr[c];
+      }
+      const int cnt = (int)min((i64)32, e1 - eb);
+      for (int q = 0; q < cnt; ++q) {  // fixed child order
+        const i64 uo = __shfl_sync(0xffffffffu, uoff, q), ro = __shfl_sync(0xffffffffu, roff, q);
+        const int lo = __shfl_sync(0xffffffffu, r_lo, q), hi = __shfl_sync(0xffffffffu, r_hi, q);
+        const double* Ucol = U + uo;
+        const int* rel = S.rel + ro;
+        for (int r = lo + lane; r < hi; r += 32) dstcol[rel[r]] += Ucol[r];
+      }
     }
-    const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
-    const int* rel = S.rel + S.relptr[c];
-    for (int r = r_lo + lane; r < r_hi; r += 32) dstcol[rel[r]] += Ucol[r];
+  } else {
+    for (i64 e = e0; e < e1; ++e) {
+      const int c = A.gchild[e];
+      const int cc = A.gsrc[e] - (int)S.Boff[c];
+      const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - (S.col0[c + 1] - S.col0[c]);
+      int r_lo = cc, r_hi = nuc;
+      if (it.band >= 0) {
+        const int* bs = A.bandstart + A.bandptr[c];
+        r_lo = max(cc, bs[it.band]);
+        r_hi = bs[it.band + 1];
+      }
+      const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+      const int* rel = S.rel + S.relptr[c];
+      for (int r = r_lo + lane; r < r_hi; r += TPR) dstcol[rel[r]] += Ucol[r];
+    }
   }
 }
 
@@ -1074,6 +1111,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
     // extend-add items per level
     std::vector<EaItem> items;
     eaptr.assign(S.nlevels + 1, 0);
+    ea_wide.clear();
     lv_tpr.assign(S.nlevels, 1);
     for (int lv = 0; lv < S.nlevels; ++lv) {
       for (i64 k = lvslot[lv]; k < lvslot[lv + 1]; ++k) {
@@ -1088,6 +1126,17 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
         }
       }
       eaptr[lv + 1] = (i64)items.size();
+      {  // mean number of update rows of the children assembled at this level decides the lanes per item
+        i64 rows = 0, kids = 0;
+        for (int k = S.levelptr[lv]; k < S.levelptr[lv + 1]; ++k) {
+          const int s2 = S.levelsup[k];
+          for (int ci = S.childptr[s2]; ci < S.childptr[s2 + 1]; ++ci) {
+            rows += S.relptr[S.child[ci] + 1] - S.relptr[S.child[ci]];
+            ++kids;
+          }
+        }
+        ea_wide.push_back(kids == 0 || rows > 16 * kids);
+      }
       const i64 ns_lv = lvslot[lv + 1] - lvslot[lv];
       const double mean = ns_lv ? (double)(gptr[lvslot[lv + 1]] - gptr[lvslot[lv]]) / (double)ns_lv : 1.0;
       int t = 1;
@@ -1194,9 +1243,14 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
     const int nslab = slabptr[lv + 1] - slabptr[lv];
     if (use_lists) {
       const i64 ni = eaptr[lv + 1] - eaptr[lv];
-      if (ni > 0)
-        k_extend_add_list<<<(unsigned)((ni * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
-            D, A, d_eaitems + eaptr[lv], ni, L, U);
+      if (ni > 0) {
+        if (ea_wide[lv])
+          k_extend_add_list<32><<<(unsigned)((ni * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+              D, A, d_eaitems + eaptr[lv], ni, L, U);
+        else
+          k_extend_add_list<4><<<(unsigned)((ni * 4 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+              D, A, d_eaitems + eaptr[lv], ni, L, U);
+      }
     } else if (nslab > 0) {
       k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
     }
