@@ -722,6 +722,16 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   if (h->have_problem) return fail(h, QS_E_INVALID, "handle already set up");
   cudaSetDevice(h->device);
   const auto t_begin = std::chrono::steady_clock::now();
+  auto t_mark = t_begin;
+  const bool verbose = getenv("QS_VERBOSE") != nullptr;
+  auto lap = [&](const char* what) {
+    if (verbose) {
+      cudaStreamSynchronize(h->stream);
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[qs setup] %-32s %8.3f s\n", what, std::chrono::duration<double>(now - t_mark).count());
+      t_mark = now;
+    }
+  };
   h->st = *settings;
   if (n < 1 || m < 1 || p < 0) return fail(h, QS_E_DIMENSION, "need n >= 1, m >= 1, p >= 0");
   int rc = qs_set_cones(h, l, nsoc, q, 0);
@@ -733,6 +743,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   h->N = n + p + m;
   const i64 N = h->N;
   cudaStream_t st = h->stream;
+  lap("cone layout + plans");
   // ---- row views
   const i64 nnzA = Ap[n], nnzG = Gp[n], nnzP = Pp[n];
   std::vector<i64> Arp(p + 1), Ari(nnzA), Grp(m + 1), Gri(nnzG);
@@ -781,6 +792,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
     hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, iota.data(), tp.data(), ti.data(), tmp.data());
     for (i64 k = 0; k < nnzG; ++k) gr_map[k] = (int)tmp[k];
   }
+  lap("row views + value maps (host)");
   h->nnzP = nnzP;
   h->nnzPf = Pfp[n];
   h->nnzA = nnzA;
@@ -809,6 +821,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
                    h->Kp_h.data(), &Kcp, &Kci);
     if (h->Kp_h[N] != h->knnz) return fail(h, QS_E_INVALID, "internal: KKT column pointers disagree with the count");
   }
+  lap("KKT column pointers + compact pattern");
   const auto t_h2d = std::chrono::steady_clock::now();
   bool ok = make_csr(h, &h->Pf, n, n, Pfp.data(), Pfi.data(), Pfx.data()) &&
             make_csr(h, &h->At, n, p, (const i64*)Ap, (const i64*)Ai, Ax) &&
@@ -886,6 +899,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
       CK(h, cudaStreamSynchronize(st));
     }
   }
+  lap("H2D of P/A/G views + device KKT fill");
   // closed-form map == explicit map?
   {
     int* flag = h->prob_pool.alloc<int>(1);
@@ -929,6 +943,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
     h->launches += 6 * h->st.ruiz_iters + 9;
   }
   h->tm.total[T_H2D] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_h2d).count();
+  lap("map check + state vectors (+ Ruiz)");
   // ---- factorisation analysis; the SOC blocks are cliques of the pattern
   std::vector<i64> cstart(nsoc), csize(nsoc);
   for (i64 k = 0; k < nsoc; ++k) {
@@ -941,6 +956,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
                                   (const i64*)user_perm, nsoc, cstart.data(), csize.data(), n, h->st.static_reg, st);
   if (!err.empty()) return fail(h, err.find("memory") != std::string::npos ? QS_E_MEMORY : QS_E_INVALID, err);
   h->tm.total[T_ANALYSIS] += h->ls.analysis_seconds;
+  lap("ordering + symbolic + LDL' setup");
   h->have_problem = true;
   (void)t_begin;
   return QS_OK;

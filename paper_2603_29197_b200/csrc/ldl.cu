@@ -4,6 +4,8 @@
 #include <cooperative_groups.h>
 
 #include <chrono>
+#include <cstdio>
+#include <thread>
 
 namespace cg = cooperative_groups;
 
@@ -885,6 +887,20 @@ __global__ void __launch_bounds__(LDL_THREADS) k_permute_out(int N, const int* p
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) sol[perm[j]] = xw[j];
 }
 
+// Host-side parallel loop over [0, n): fn(lo, hi) on up to 8 threads (the analysis runs once per problem; its loops
+// over 10^6 supernodes / 10^7 list entries are memory-bound and independent per parent).
+template <class Fn>
+void parallel_ranges(i64 n, Fn fn) {
+  const int nt = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < 200000 || nt == 1) {
+    fn((i64)0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(fn, n * t / nt, n * (t + 1) / nt);
+  for (auto& th : pool) th.join();
+}
+
 template <class... Args>
 void launch_clustered(void (*kern)(Args...), int nfronts, int cl, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -934,6 +950,17 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   knnz = knnz_full;
   std::string err = hs_symbolic_cliques(N, Kp, Ki, order, user_perm, ncliques, clique_start, clique_size, &S);
   if (!err.empty()) return err;
+  const bool verbose = getenv("QS_VERBOSE") != nullptr;
+  auto t_mark = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (verbose) {
+      cudaStreamSynchronize(st);
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[qs ldl setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t_mark).count());
+      t_mark = now;
+    }
+  };
+  lap("(symbolic total)");
   D.nsup = S.nsup;
 #define UP(field, vec)                                   \
   D.field = upload(vec, &owned, &device_bytes, st);      \
@@ -1032,53 +1059,59 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   device_bytes += pmax * 8;
   d_slabs = upload(slabs, &owned, &device_bytes, st);
   if (!d_leaf || !d_gen || !d_small || !d_blk || !d_slabs) return "cudaMalloc failed for LDL work lists";
+  lap("symbolic upload + work lists");
   // ---- assembly lists (AsmLists): slots of the fronts that have children, level by level
   use_cluster = getenv("QS_LDL_LOCKSTEP") == nullptr;
   use_graphs = getenv("QS_NO_GRAPH") == nullptr;
   use_lists = getenv("QS_LDL_SEARCH") == nullptr && S.Boff[S.nsup] < ((i64)1 << 31);
   if (use_lists) {
     std::vector<i64> slot_base(S.nsup, -1);
-    std::vector<int> slot_front, slot_row;
     lvslot.assign(S.nlevels + 1, 0);
+    i64 nslots = 0;
     for (int lv = 0; lv < S.nlevels; ++lv) {
       for (int k = S.levelptr[lv]; k < S.levelptr[lv + 1]; ++k) {
         const int s = S.levelsup[k];
         if (S.childptr[s + 1] == S.childptr[s]) continue;
-        const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
-        slot_base[s] = (i64)slot_front.size();
+        slot_base[s] = nslots;
+        nslots += S.rowptr[s + 1] - S.rowptr[s];
+      }
+      lvslot[lv + 1] = nslots;
+    }
+    std::vector<int> slot_front(nslots), slot_row(nslots);
+    std::vector<i64> gptr(nslots + 1, 0), gdst(nslots);
+    // every loop below is partitioned by PARENT supernode: a thread touches only the slots of its own parents
+    parallel_ranges(S.nsup, [&](i64 lo, i64 hi) {
+      for (i64 s = lo; s < hi; ++s) {
+        if (slot_base[s] < 0) continue;
+        const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]), ns = S.col0[s + 1] - S.col0[s];
         for (int r = 0; r < nr; ++r) {
-          slot_front.push_back(s);
-          slot_row.push_back(r);
+          const i64 k = slot_base[s] + r;
+          slot_front[k] = (int)s;
+          slot_row[k] = r;
+          gdst[k] = (r < ns) ? (i64)(S.col0[s] + r) : -(S.Boff[s] + (r - ns)) - 1;
+        }
+        for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci) {
+          const int c = S.child[ci];
+          for (i64 t = S.relptr[c]; t < S.relptr[c + 1]; ++t) gptr[slot_base[s] + S.rel[t] + 1]++;
         }
       }
-      lvslot[lv + 1] = (i64)slot_front.size();
-    }
-    const i64 nslots = (i64)slot_front.size();
-    std::vector<i64> gptr(nslots + 1, 0), gdst(nslots);
-    for (int c = 0; c < S.nsup; ++c) {
-      const int par = S.parent[c];
-      if (par < 0) continue;
-      for (i64 t = S.relptr[c]; t < S.relptr[c + 1]; ++t) gptr[slot_base[par] + S.rel[t] + 1]++;
-    }
+    });
     for (i64 k = 0; k < nslots; ++k) gptr[k + 1] += gptr[k];
     std::vector<int> gsrc(gptr[nslots]), gchild(gptr[nslots]);
     {
       std::vector<i64> next(gptr.begin(), gptr.end() - 1);
-      for (int s = 0; s < S.nsup; ++s)  // children in their fixed (ascending) order
-        for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci) {
-          const int c = S.child[ci];
-          const i64 nuc = S.relptr[c + 1] - S.relptr[c];
-          for (i64 t = 0; t < nuc; ++t) {
-            const i64 e = next[slot_base[s] + S.rel[S.relptr[c] + t]]++;
-            gsrc[e] = (int)(S.Boff[c] + t);
-            gchild[e] = c;
+      parallel_ranges(S.nsup, [&](i64 lo, i64 hi) {
+        for (i64 s = lo; s < hi; ++s)  // children in their fixed (ascending) order
+          for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci) {
+            const int c = S.child[ci];
+            const i64 nuc = S.relptr[c + 1] - S.relptr[c];
+            for (i64 t = 0; t < nuc; ++t) {
+              const i64 e = next[slot_base[s] + S.rel[S.relptr[c] + t]]++;
+              gsrc[e] = (int)(S.Boff[c] + t);
+              gchild[e] = c;
+            }
           }
-        }
-    }
-    for (i64 k = 0; k < nslots; ++k) {
-      const int s = slot_front[k], r = slot_row[k];
-      const int ns = S.col0[s + 1] - S.col0[s];
-      gdst[k] = (r < ns) ? (i64)(S.col0[s] + r) : -(S.Boff[s] + (r - ns)) - 1;
+      });
     }
     // row bands for fronts with many children
     std::vector<i64> bandptr(S.nsup + 1, 0);
@@ -1161,6 +1194,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
       cudaStreamSynchronize(st);  // the host vectors above die at the end of this block
     }
   }
+  lap("assembly lists");
   std::vector<double> regh(N);
   for (i64 k = 0; k < N; ++k) regh[k] = (S.perm[k] < n_pos) ? static_reg : -static_reg;  // kkt.py:48-52
   reg = upload(regh, &owned, &device_bytes, st);
@@ -1182,6 +1216,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
                                                                                               amap);
   cudaStreamSynchronize(st);  // host vectors above must outlive the async copies
   if (cudaGetLastError() != cudaSuccess) return "LDL' analysis kernels failed";
+  lap("factor storage + amap");
   h2d_bytes = g_upload_bytes - upload_mark;
   analysis_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return std::string();
