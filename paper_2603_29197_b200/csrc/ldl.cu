@@ -271,47 +271,66 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 // One CTA per front of the level (children already assembled by k_extend_add):
 // factor the pivot panel, form this front's own update matrix.
-__global__ void __launch_bounds__(LDL_THREADS)
-    k_front_factor(DevSym S, const int* list, double* L, double* U, double* Dg, const double* reg, double dyn_eps,
-                   double* scalars) {
-  const int s = list[blockIdx.x];
+// Small fronts (at most QS_SMALL_NR rows and QS_SMALL_NS pivots: the panel is <= 36 KB) are factored IN SHARED MEMORY:
+// one coalesced load of the panel, every pivot step at shared-memory latency, one coalesced store; the update matrix
+// is then formed from the shared copy.  (In global memory every one of the ~2 ns barrier-separated steps paid an L2
+// round trip; a chain of 100 small fronts is bound by exactly that latency.)
+#define QS_SMALL_NR 96
+#define QS_SMALL_NS 48
+
+__device__ void front_factor_body(const DevSym& S, int s, double* L, double* U, double* Dg, const double* reg,
+                                  double dyn_eps, double* scalars) {
+  __shared__ double Ls[QS_SMALL_NR * QS_SMALL_NS];
+  __shared__ double dsm[QS_SMALL_NS];
   const Front f = front_of(S, s, L, U);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const i64 nr = f.nr, nu = f.nu;
+  const int nr = f.nr, ns = f.ns, nu = f.nu;
+  __syncthreads();  // the shared arrays may still be read by the previous front of a chain
+  for (int e = tid; e < nr * ns; e += blockDim.x) Ls[e] = f.Lp[e];
   // ---- right-looking LDL' on the pivot panel (nr x ns)
-  for (int k = 0; k < f.ns; ++k) {
+  for (int k = 0; k < ns; ++k) {
     __syncthreads();
-    double d = f.Lp[k + k * nr];
+    double d = Ls[k + k * nr];
     if (!qs_finite(d)) {
       if (tid == 0) scalars[SC_PIVOT_NONFINITE] = 1.0;
     } else if (fabs(d) < dyn_eps) {  // dynamic floor, sign from the expected inertia (_kernels.py:160-165)
       d = (reg[f.c0 + k] >= 0.0) ? dyn_eps : -dyn_eps;
       if (tid == 0) atomicAdd(&scalars[SC_PIVOT_BUMPS], 1.0);
     }
-    if (tid == 0) Dg[f.c0 + k] = d;
-    for (int j = k + 1 + warp; j < f.ns; j += nwarps) {
-      const double ljk = f.Lp[j + k * nr] / d;
-      for (int i = j + lane; i < f.nr; i += 32) f.Lp[i + j * nr] -= f.Lp[i + k * nr] * ljk;
+    if (tid == 0) {
+      Dg[f.c0 + k] = d;
+      dsm[k] = d;
+    }
+    for (int j = k + 1 + warp; j < ns; j += nwarps) {
+      const double ljk = Ls[j + k * nr] / d;
+      for (int i = j + lane; i < nr; i += 32) Ls[i + j * nr] -= Ls[i + k * nr] * ljk;
     }
     __syncthreads();
-    for (int i = k + 1 + tid; i < f.nr; i += blockDim.x) f.Lp[i + k * nr] /= d;
+    for (int i = k + 1 + tid; i < nr; i += blockDim.x) Ls[i + k * nr] /= d;
   }
   __syncthreads();
+  for (int e = tid; e < nr * ns; e += blockDim.x) f.Lp[e] = Ls[e];
   // ---- update matrix: U -= L21 D L21'
-  if (f.nu > 0) {
-    const double* L21 = f.Lp + f.ns;
-    for (int j = warp; j < f.nu; j += nwarps) {
-      for (int i0 = j; i0 < f.nu; i0 += 32) {
+  if (nu > 0) {
+    const double* L21 = Ls + ns;
+    for (int j = warp; j < nu; j += nwarps) {
+      for (int i0 = j; i0 < nu; i0 += 32) {
         const int i = i0 + lane;
         double acc = 0.0;
-        for (int k = 0; k < f.ns; ++k) {
-          const double t = L21[j + k * nr] * Dg[f.c0 + k];
-          if (i < f.nu) acc += L21[i + k * nr] * t;
+        for (int k = 0; k < ns; ++k) {
+          const double t = L21[j + k * nr] * dsm[k];
+          if (i < nu) acc += L21[i + k * nr] * t;
         }
-        if (i < f.nu) f.Up[i + j * nu] -= acc;
+        if (i < nu) f.Up[i + (i64)j * nu] -= acc;
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_front_factor(DevSym S, const int* list, double* L, double* U, double* Dg, const double* reg, double dyn_eps,
+                   double* scalars) {
+  front_factor_body(S, list[blockIdx.x], L, U, Dg, reg, dyn_eps, scalars);
 }
 
 // ============================ blocked path for large fronts ==================
@@ -828,56 +847,138 @@ __global__ void __launch_bounds__(LDL_THREADS)
 }
 
 // ---- triangular solves, one CTA per front of the level
-__global__ void __launch_bounds__(LDL_THREADS)
-    k_solve_fwd(DevSym S, const int* list, const double* L, double* xw, double* B) {
-  const int s = list[blockIdx.x];
+__device__ void solve_fwd_body(const DevSym& S, int s, const double* L, double* xw, double* B) {
+  __shared__ double L11[QS_SMALL_NS * QS_SMALL_NS];
+  __shared__ double xs[QS_SMALL_NS];
   const Front f = front_of(S, s, const_cast<double*>(L), nullptr);
   const int tid = threadIdx.x;
-  const i64 nr = f.nr;
+  const int nr = f.nr, ns = f.ns;
   double* cb = B + S.Boff[s];
-  if (S.childptr[s + 1] == S.childptr[s]) {  // no children: nothing was gathered, start from zero
-    for (int r = tid; r < f.nu; r += blockDim.x) cb[r] = 0.0;
-    __syncthreads();
-  }
+  const bool childless = S.childptr[s + 1] == S.childptr[s];  // nothing was gathered: start from zero
   double* x1 = xw + f.c0;
-  for (int k = 0; k < f.ns - 1; ++k) {
-    const double xk = x1[k];
-    for (int i = k + 1 + tid; i < f.ns; i += blockDim.x) x1[i] -= f.Lp[i + k * nr] * xk;
+  __syncthreads();  // shared arrays may still be read by the previous front of a chain
+  for (int e = tid; e < ns * ns; e += blockDim.x) L11[e] = f.Lp[(e % ns) + (i64)(e / ns) * nr];
+  if (tid < ns) xs[tid] = x1[tid];
+  __syncthreads();
+  for (int k = 0; k < ns - 1; ++k) {  // unit lower triangular solve at shared-memory latency
+    const double xk = xs[k];
+    for (int i = k + 1 + tid; i < ns; i += blockDim.x) xs[i] -= L11[i + k * ns] * xk;
     __syncthreads();
   }
-  __syncthreads();
+  if (tid < ns) x1[tid] = xs[tid];
   for (int r = tid; r < f.nu; r += blockDim.x) {
     double acc = 0.0;
-    for (int k = 0; k < f.ns; ++k) acc += f.Lp[f.ns + r + k * nr] * x1[k];
-    cb[r] -= acc;
+    for (int k = 0; k < ns; ++k) acc += f.Lp[ns + r + (i64)k * nr] * xs[k];
+    cb[r] = (childless ? 0.0 : cb[r]) - acc;
   }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_solve_fwd(DevSym S, const int* list, const double* L, double* xw, double* B) {
+  solve_fwd_body(S, list[blockIdx.x], L, xw, B);
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_solve_diag(int N, const double* Dg, double* xw) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) xw[j] /= Dg[j];
 }
 
-__global__ void __launch_bounds__(LDL_THREADS) k_solve_bwd(DevSym S, const int* list, const double* L, double* xw) {
-  const int s = list[blockIdx.x];
+__device__ void solve_bwd_body(const DevSym& S, int s, const double* L, double* xw) {
+  __shared__ double L11[QS_SMALL_NS * QS_SMALL_NS];
+  __shared__ double xs[QS_SMALL_NS];
   const Front f = front_of(S, s, const_cast<double*>(L), nullptr);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const i64 nr = f.nr;
+  const int nr = f.nr, ns = f.ns;
   double* x1 = xw + f.c0;
+  __syncthreads();  // shared arrays may still be read by the previous front of a chain
+  for (int e = tid; e < ns * ns; e += blockDim.x) L11[e] = f.Lp[(e % ns) + (i64)(e / ns) * nr];
   // x1 -= L21' x2
-  for (int k = warp; k < f.ns; k += nwarps) {
+  for (int k = warp; k < ns; k += nwarps) {
     double acc = 0.0;
-    for (int r = lane; r < f.nu; r += 32) acc += f.Lp[f.ns + r + k * nr] * xw[f.rows[f.ns + r]];
+    for (int r = lane; r < f.nu; r += 32) acc += f.Lp[ns + r + (i64)k * nr] * xw[f.rows[ns + r]];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x1[k] -= acc;
+    if (lane == 0) xs[k] = x1[k] - acc;
   }
   __syncthreads();
   // x1 <- L11^{-T} x1
-  for (int k = f.ns - 1; k > 0; --k) {
-    const double xk = x1[k];
-    for (int i = tid; i < k; i += blockDim.x) x1[i] -= f.Lp[k + i * nr] * xk;
+  for (int k = ns - 1; k > 0; --k) {
+    const double xk = xs[k];
+    for (int i = tid; i < k; i += blockDim.x) xs[i] -= L11[k + i * ns] * xk;
     __syncthreads();
   }
+  if (tid < ns) x1[tid] = xs[tid];
+}
+
+__global__ void __launch_bounds__(LDL_THREADS) k_solve_bwd(DevSym S, const int* list, const double* L, double* xw) {
+  solve_bwd_body(S, list[blockIdx.x], L, xw);
+}
+
+// ---- narrow-level chains (the upper part of the elimination tree of a banded / staged problem such as an MPC
+// trajectory is a long chain of small fronts, one or two per level): ONE CTA walks a run of consecutive narrow levels,
+// barriers between the steps, instead of 3-5 launches per level -- a small problem is bound by the number of
+// dependent launches, not by bytes or flops.
+struct ChainArgs {
+  int lv0, lv1;             // levels [lv0, lv1)
+  const int* smallptr;      // [nlevels+1] offsets into small_list
+  const int* small_list;
+  const i64* eaptr;         // [nlevels+1] extend-add item ranges
+  const EaItem* eaitems;
+  const i64* lvslot;        // [nlevels+1] slot ranges
+};
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_chain_factor(DevSym S, AsmLists A, ChainArgs C, double* L, double* U, double* Dg, const double* reg, double dyn_eps,
+                   double* scalars) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int lv = C.lv0; lv < C.lv1; ++lv) {
+    // extend-add of the level: a warp per (column slot) item, children in list order
+    for (i64 w = C.eaptr[lv] + warp; w < C.eaptr[lv + 1]; w += nwarps) {
+      const EaItem it = C.eaitems[w];
+      const int s = A.slot_front[it.slot], pc = A.slot_row[it.slot];
+      const Front f = front_of(S, s, L, U);
+      const i64 nr = f.nr, nu = f.nu;
+      double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;
+      for (i64 e = A.gptr[it.slot]; e < A.gptr[it.slot + 1]; ++e) {
+        const int c = A.gchild[e];
+        const int cc = A.gsrc[e] - (int)S.Boff[c];
+        const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - (S.col0[c + 1] - S.col0[c]);
+        const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+        const int* rel = S.rel + S.relptr[c];
+        for (int r = cc + lane; r < nuc; r += 32) dstcol[rel[r]] += Ucol[r];
+      }
+    }
+    __syncthreads();
+    for (int k = C.smallptr[lv]; k < C.smallptr[lv + 1]; ++k) {
+      front_factor_body(S, C.small_list[k], L, U, Dg, reg, dyn_eps, scalars);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS)
+    k_chain_fwd(DevSym S, AsmLists A, ChainArgs C, const double* L, double* xw, double* B) {
+  for (int lv = C.lv0; lv < C.lv1; ++lv) {
+    for (i64 g = C.lvslot[lv] + threadIdx.x; g < C.lvslot[lv + 1]; g += blockDim.x) {  // thread per slot
+      double acc = 0.0;
+      for (i64 e = A.gptr[g]; e < A.gptr[g + 1]; ++e) acc += B[A.gsrc[e]];
+      const i64 d = A.gdst[g];
+      if (d >= 0) xw[d] += acc;
+      else B[-d - 1] = acc;
+    }
+    __syncthreads();
+    for (int k = C.smallptr[lv]; k < C.smallptr[lv + 1]; ++k) {
+      solve_fwd_body(S, C.small_list[k], L, xw, B);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(LDL_THREADS) k_chain_bwd(DevSym S, ChainArgs C, const double* L, double* xw) {
+  for (int lv = C.lv1 - 1; lv >= C.lv0; --lv)
+    for (int k = C.smallptr[lv]; k < C.smallptr[lv + 1]; ++k) {
+      solve_bwd_body(S, C.small_list[k], L, xw);
+      __syncthreads();
+    }
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_permute_in(int N, const int* perm, const double* rhs, double* xw) {
@@ -1002,7 +1103,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
         continue;
       }
       gen.push_back(s);
-      if (nr > 96 || ns > 48) {
+      if (nr > QS_SMALL_NR || ns > QS_SMALL_NS) {
         blk.push_back(s);
         blk_max_ns[lv] = std::max(blk_max_ns[lv], ns);
         blk_max_nr[lv] = std::max(blk_max_nr[lv], nr);
@@ -1194,6 +1295,34 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
       cudaStreamSynchronize(st);  // the host vectors above die at the end of this block
     }
   }
+  // ---- narrow-level chains: maximal runs of >= 3 consecutive levels that hold only a few small fronts each
+  chain_end.assign(S.nlevels, 0);
+  chain_start_of_end.assign(S.nlevels, -1);
+  for (int lv = 0; lv < S.nlevels; ++lv) chain_end[lv] = lv + 1;
+  if (use_lists && getenv("QS_LDL_NO_CHAIN") == nullptr) {
+    auto narrow = [&](int lv) {
+      const int nsm = smallptr[lv + 1] - smallptr[lv];
+      return lv > 0 && blkptr[lv + 1] == blkptr[lv] && nsm >= 1 && nsm <= 8 && lvslot[lv + 1] - lvslot[lv] <= 4096;
+    };
+    for (int lv = 0; lv < S.nlevels;) {
+      int e = lv;
+      while (e < S.nlevels && narrow(e)) ++e;
+      if (e - lv >= 3) {
+        chain_end[lv] = e;
+        lv = e;
+      } else {
+        lv = std::max(e, lv + 1);
+      }
+    }
+    chain_start_of_end.assign(S.nlevels, -1);
+    for (int lv = 0; lv < S.nlevels; ++lv)
+      if (chain_end[lv] > lv + 1) chain_start_of_end[chain_end[lv] - 1] = lv;
+    d_smallptr = upload(smallptr, &owned, &device_bytes, st);
+    d_eaptr = upload(eaptr, &owned, &device_bytes, st);
+    d_lvslot = upload(lvslot, &owned, &device_bytes, st);
+    if (!d_smallptr || !d_eaptr || !d_lvslot) return "cudaMalloc failed for the chain tables";
+    cudaStreamSynchronize(st);
+  }
   lap("assembly lists");
   std::vector<double> regh(N);
   for (i64 k = 0; k < N; ++k) regh[k] = (S.perm[k] < n_pos) ? static_reg : -static_reg;  // kkt.py:48-52
@@ -1275,6 +1404,12 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
     k_leaf_factor<<<(unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
         D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars);
   for (int lv = 0; lv < S.nlevels; ++lv) {
+    if (chain_end[lv] > lv + 1) {  // a run of narrow levels: one single-CTA launch
+      const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
+      k_chain_factor<<<1, LDL_THREADS, 0, st>>>(D, A, C, L, U, Dg, reg, dyn_eps, scalars);
+      lv = chain_end[lv] - 1;
+      continue;
+    }
     const int nslab = slabptr[lv + 1] - slabptr[lv];
     if (use_lists) {
       const i64 ni = eaptr[lv + 1] - eaptr[lv];
@@ -1335,6 +1470,12 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
   const unsigned leaf_grid = (unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS);
   if (n_leaf > 0) k_leaf_fwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw, B);
   for (int lv = 0; lv < S.nlevels; ++lv) {
+    if (chain_end[lv] > lv + 1) {
+      const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
+      k_chain_fwd<<<1, LDL_THREADS, 0, st>>>(D, A, C, L, xw, B);
+      lv = chain_end[lv] - 1;
+      continue;
+    }
     const int nslab = slabptr[lv + 1] - slabptr[lv];
     if (use_lists) {
       const i64 nsl = lvslot[lv + 1] - lvslot[lv];
@@ -1369,7 +1510,15 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
     }
   }
   k_solve_diag<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, Dg, xw);
+  // chain_start[e - 1] = first level of the chain that ends at level e - 1 (or -1)
   for (int lv = S.nlevels - 1; lv >= 0; --lv) {
+    if (chain_start_of_end[lv] >= 0) {
+      const int b = chain_start_of_end[lv];
+      const ChainArgs C{b, lv + 1, d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
+      k_chain_bwd<<<1, LDL_THREADS, 0, st>>>(D, C, L, xw);
+      lv = b;
+      continue;
+    }
     const int nblk_lv = blkptr[lv + 1] - blkptr[lv];
     const bool clustered = use_cluster && nblk_lv > 0 && nblk_lv <= 16;
     if (clustered)
@@ -1399,6 +1548,11 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
 int LinSys::launches_per_factor() const {
   int k = 2 + (n_leaf > 0);  // own kernels only (the two memsets are not counted)
   for (int lv = 0; lv < S.nlevels; ++lv) {
+    if (chain_end[lv] > lv + 1) {
+      k += 1;
+      lv = chain_end[lv] - 1;
+      continue;
+    }
     k += (slabptr[lv + 1] > slabptr[lv]) + (smallptr[lv + 1] > smallptr[lv]);
     if (blkptr[lv + 1] > blkptr[lv]) {
       const int chunks = (blkptr[lv + 1] - blkptr[lv] + 65534) / 65535;
@@ -1411,6 +1565,11 @@ int LinSys::launches_per_factor() const {
 int LinSys::launches_per_solve() const {
   int k = 3 + 2 * (n_leaf > 0);
   for (int lv = 0; lv < S.nlevels; ++lv) {
+    if (chain_end[lv] > lv + 1) {
+      k += 2;
+      lv = chain_end[lv] - 1;
+      continue;
+    }
     k += (slabptr[lv + 1] > slabptr[lv]) + 2 * (smallptr[lv + 1] > smallptr[lv]);
     const int nblk_lv = blkptr[lv + 1] - blkptr[lv];
     if (use_cluster && nblk_lv > 0 && nblk_lv <= 16) {

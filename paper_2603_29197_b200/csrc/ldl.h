@@ -129,6 +129,11 @@ struct LinSys {
   };
   std::vector<GraphEntry> factor_graphs, solve_graphs;
   bool use_graphs = true;
+  // narrow-level chains: chain_end[lv] > lv + 1 when levels [lv, chain_end[lv]) are fused into one single-CTA launch
+  std::vector<int> chain_end, chain_start_of_end;
+  int* d_smallptr = nullptr;
+  i64* d_eaptr = nullptr;
+  i64* d_lvslot = nullptr;
   int launches_per_factor() const;
   int launches_per_solve() const;
   void release();
