@@ -863,6 +863,24 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
     for (int s = 0; s < nsup; ++s) {
       const int c0 = S->col0[s], c1 = S->col0[s + 1];
       const size_t begin = S->rowidx.size();
+      if (c1 - c0 == 1 && S->childptr[s + 1] == S->childptr[s]) {
+        // one-column leaf (the 1.35 M private x-columns of C4): its rows are its own lower pattern, which `li`
+        // already lists in ascending order without repeats -- no marking, no sort
+        S->rowidx.push_back(c0);
+        bool ascending = true;
+        int prev = c0;
+        for (i64 k = lp[c0]; k < lp[c0 + 1]; ++k) {
+          ascending = ascending && li[k] > prev;
+          prev = li[k];
+          S->rowidx.push_back(li[k]);
+        }
+        if (ascending) {
+          S->rowptr[s + 1] = (i64)S->rowidx.size();
+          if ((i64)(S->rowidx.size() - begin) < cc[c0]) return "internal: front smaller than its first column count";
+          continue;
+        }
+        S->rowidx.resize(begin);  // repeated entries in the pattern: take the general path
+      }
       for (int c = c0; c < c1; ++c) {
         mark[c] = s;
         S->rowidx.push_back(c);
