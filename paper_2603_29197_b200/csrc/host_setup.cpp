@@ -801,6 +801,7 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
   double relax = 0.4;
   if (const char* e = getenv("QS_RELAX")) relax = atof(e);
   i64 g_ns = 0, g_nr = 0, g_zeros = 0;  // current group: columns, front rows, padded zeros
+  std::vector<i64> nr_of;               // front rows of every group (supernode)
   for (i64 j = 0; j < N; ++j) {
     bool merge = false;
     if (j > 0 && parent[j - 1] == j) {
@@ -814,6 +815,7 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
         g_zeros = zeros;
         g_nr = nr_new;
         g_ns += 1;
+        nr_of.back() = g_nr;
       }
     }
     if (!merge) {
@@ -821,6 +823,7 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
       g_ns = 1;
       g_nr = cc[j];
       g_zeros = 0;
+      nr_of.push_back(g_nr);
     }
     S->sup_of[j] = (int)S->col0.size() - 1;
   }
@@ -845,7 +848,116 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
       if (S->parent[s] >= 0) S->child[next[S->parent[s]]++] = s;
   }
 
-  // 5. front row structures, bottom-up (children precede parents)
+  // 5. front row structures.  The row COUNT of every front is known from the grouping pass (nr_of), so the storage
+  // is laid out first and the fronts of one tree level -- independent of each other, children one level down already
+  // done -- are filled by host threads with private marker arrays.  Any count mismatch falls back to the sequential
+  // bottom-up pass below.
+  bool fronts_done = false;
+  {
+    std::vector<int> lev(nsup, 0);
+    int nlev = 1;
+    for (int s = 0; s < nsup; ++s) {  // children precede parents
+      const int par = S->parent[s];
+      if (par >= 0) lev[par] = std::max(lev[par], lev[s] + 1);
+      nlev = std::max(nlev, lev[s] + 1);
+    }
+    const int nthreads = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (nsup >= 100000 && nthreads > 1 && nlev <= 64) {
+      std::vector<int> lptr(nlev + 1, 0), lsup(nsup);
+      for (int s = 0; s < nsup; ++s) lptr[lev[s] + 1]++;
+      for (int v = 0; v < nlev; ++v) lptr[v + 1] += lptr[v];
+      {
+        std::vector<int> next(lptr.begin(), lptr.end() - 1);
+        for (int s = 0; s < nsup; ++s) lsup[next[lev[s]]++] = s;
+      }
+      lap("  level buckets");
+      S->rowptr.assign(nsup + 1, 0);
+      for (int s = 0; s < nsup; ++s) S->rowptr[s + 1] = S->rowptr[s] + nr_of[s];
+      S->rowidx.assign(S->rowptr[nsup], 0);
+      lap("  row storage");
+      // lower pattern by column = transpose of B.  Every thread streams all of B but counts / writes only the
+      // destination columns of its own range: sequential reads, private writes, no atomics, same order as serial.
+      std::vector<i64> lp(N + 1, 0);
+      auto split = [&](auto fn) {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nthreads; ++t) pool.emplace_back(fn, (int)(N * t / nthreads), (int)(N * (t + 1) / nthreads));
+        for (auto& th : pool) th.join();
+      };
+      split([&](int lo, int hi) {
+        for (i64 j = 0; j < N; ++j)
+          for (i64 k = B.ptr[j]; k < B.ptr[j + 1]; ++k) {
+            const int r = B.row[k];
+            if (r >= lo && r < hi) lp[r + 1]++;
+          }
+      });
+      lap("  transpose: count");
+      for (i64 v = 0; v < N; ++v) lp[v + 1] += lp[v];
+      std::vector<int> li(lp[N]);
+      {
+        std::vector<i64> next(lp.begin(), lp.end() - 1);
+        split([&](int lo, int hi) {
+          for (i64 j = 0; j < N; ++j)
+            for (i64 k = B.ptr[j]; k < B.ptr[j + 1]; ++k) {
+              const int r = B.row[k];
+              if (r >= lo && r < hi) li[next[r]++] = (int)j;
+            }
+        });
+      }
+      lap("  lower pattern by column");
+      std::atomic<bool> mismatch{false};
+      std::vector<std::vector<int>> marks(nthreads);
+      for (int v = 0; v < nlev && !mismatch; ++v) {
+        const int cnt = lptr[v + 1] - lptr[v];
+        const int use = cnt >= 4096 ? nthreads : 1;
+        auto work = [&](int t) {
+          std::vector<int>& mark = marks[t];
+          if (mark.empty()) mark.assign(N, -1);
+          for (int q = lptr[v] + (int)((i64)cnt * t / use); q < lptr[v] + (int)((i64)cnt * (t + 1) / use); ++q) {
+            const int s = lsup[q];
+            const int c0 = S->col0[s], c1 = S->col0[s + 1];
+            int* out = S->rowidx.data() + S->rowptr[s];
+            const i64 cap = nr_of[s];
+            i64 at = 0;
+            for (int c = c0; c < c1; ++c) {
+              mark[c] = s;
+              if (at < cap) out[at] = c;
+              ++at;
+            }
+            auto add = [&](int r) {
+              if (r >= c1 && mark[r] != s) {
+                mark[r] = s;
+                if (at < cap) out[at] = r;
+                ++at;
+              }
+            };
+            for (int c = c0; c < c1; ++c)
+              for (i64 k = lp[c]; k < lp[c + 1]; ++k) add(li[k]);
+            for (int ci = S->childptr[s]; ci < S->childptr[s + 1]; ++ci) {
+              const int ch = S->child[ci];
+              const int nsc = S->col0[ch + 1] - S->col0[ch];
+              for (i64 k = S->rowptr[ch] + nsc; k < S->rowptr[ch + 1]; ++k) add(S->rowidx[k]);
+            }
+            if (at != cap) {
+              mismatch = true;
+              return;
+            }
+            std::sort(out + (c1 - c0), out + cap);
+          }
+        };
+        if (use == 1) {
+          work(0);
+        } else {
+          std::vector<std::thread> pool;
+          for (int t = 0; t < use; ++t) pool.emplace_back(work, t);
+          for (auto& th : pool) th.join();
+        }
+      }
+      fronts_done = !mismatch;
+      lap(fronts_done ? "  fronts by level (threaded)" : "  fronts by level: count mismatch");
+    }
+  }
+  if (!fronts_done) {
+  // sequential bottom-up pass (children precede parents)
   S->rowptr.assign(nsup + 1, 0);
   S->rowidx.clear();
   S->rowidx.reserve((size_t)N * 4);
@@ -902,6 +1014,7 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
       S->rowptr[s + 1] = (i64)S->rowidx.size();
       if ((i64)(S->rowidx.size() - begin) < cc[c0]) return "internal: front smaller than its first column count";
     }
+  }
   }
   lap("front structures");
   // 6. relative indices, storage offsets, levels, statistics
