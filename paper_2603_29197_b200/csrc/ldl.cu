@@ -138,12 +138,13 @@ __global__ void __launch_bounds__(LDL_THREADS)
 // (children with a handful of update rows, e.g. the 1.35 M one-column leaves of C4): eight items per warp.
 template <int TPR>
 __global__ void __launch_bounds__(LDL_THREADS)
-    k_extend_add_list(DevSym S, AsmLists A, const EaItem* items, i64 nitems, double* L, double* U) {
+    k_extend_add_list(DevSym S, AsmLists A, const EaItem* items, i64 slot0, i64 nitems, double* L, double* U) {
   const i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / TPR;
   const int lane = threadIdx.x & (TPR - 1);
   if (TPR == 32 ? w >= nitems : false) return;
   const bool on = w < nitems;
-  const EaItem it = on ? items[w] : EaItem{0, -1};
+  // items == nullptr: the level has no banded front, item w is simply column slot slot0 + w (whole column)
+  const EaItem it = on ? (items ? items[w] : EaItem{(int)(slot0 + w), -1}) : EaItem{(int)slot0, -1};
   const int s = A.slot_front[it.slot], pc = A.slot_row[it.slot];
   const Front f = front_of(S, s, L, U);
   const i64 nr = f.nr, nu = f.nu;
@@ -1178,6 +1179,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
       }
       lvslot[lv + 1] = nslots;
     }
+    lap("  lists: slot bases");
     std::vector<int> slot_front(nslots), slot_row(nslots);
     std::vector<i64> gptr(nslots + 1, 0), gdst(nslots);
     // every loop below is partitioned by PARENT supernode: a thread touches only the slots of its own parents
@@ -1197,6 +1199,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
         }
       }
     });
+    lap("  lists: slots + counts");
     for (i64 k = 0; k < nslots; ++k) gptr[k + 1] += gptr[k];
     std::vector<int> gsrc(gptr[nslots]), gchild(gptr[nslots]);
     {
@@ -1214,12 +1217,19 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
           }
       });
     }
+    lap("  lists: fill");
     // row bands for fronts with many children
     std::vector<i64> bandptr(S.nsup + 1, 0);
     std::vector<char> banded(S.nsup, 0);
     for (int s = 0; s < S.nsup; ++s) {
       const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]);
-      banded[s] = (S.childptr[s + 1] - S.childptr[s] >= 64 && nr > QS_EA_BAND);
+      // bands pay off when many children each bring many rows (the root: 10^4 children x ~400 rows); a cone
+      // front with 135 one-column leaves of 4 rows gains nothing from them
+      i64 child_rows = 0;
+      const int nch = S.childptr[s + 1] - S.childptr[s];
+      for (int ci = S.childptr[s]; ci < S.childptr[s + 1]; ++ci)
+        child_rows += S.relptr[S.child[ci] + 1] - S.relptr[S.child[ci]];
+      banded[s] = (nch >= 64 && nr > QS_EA_BAND && child_rows > 32 * (i64)nch);
     }
     for (int c = 0; c < S.nsup; ++c) {
       const int par = S.parent[c];
@@ -1242,13 +1252,21 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
         bandstart[bandptr[c] + b] = r;
       }
     }
+    lap("  lists: bands");
     // extend-add items per level
     std::vector<EaItem> items;
     eaptr.assign(S.nlevels + 1, 0);
     ea_wide.clear();
     lv_tpr.assign(S.nlevels, 1);
+    ea_direct.assign(S.nlevels, 0);
+    items.reserve(1 << 16);
     for (int lv = 0; lv < S.nlevels; ++lv) {
-      for (i64 k = lvslot[lv]; k < lvslot[lv + 1]; ++k) {
+      // a wide level without banded fronts needs no item list: item w is column slot lvslot[lv] + w (an explicit
+      // list would be 8 bytes x 7 M slots at C4, built and uploaded for nothing)
+      bool any_banded = false;
+      for (int k = S.levelptr[lv]; k < S.levelptr[lv + 1] && !any_banded; ++k) any_banded = banded[S.levelsup[k]];
+      ea_direct[lv] = !any_banded && lvslot[lv + 1] - lvslot[lv] > 4096;
+      for (i64 k = lvslot[lv]; k < lvslot[lv + 1] && !ea_direct[lv]; ++k) {
         if (gptr[k + 1] == gptr[k]) continue;  // nothing lands on this column
         const int s = slot_front[k];
         if (!banded[s]) {
@@ -1277,6 +1295,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
       while (t < 32 && t * 2 <= mean) t <<= 1;
       lv_tpr[lv] = t;
     }
+    lap("  lists: items + lanes");
     if (nslots >= ((i64)1 << 31)) {
       use_lists = false;
     } else {
@@ -1295,6 +1314,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
       cudaStreamSynchronize(st);  // the host vectors above die at the end of this block
     }
   }
+  lap("  lists: uploads");
   // ---- narrow-level chains: maximal runs of >= 3 consecutive levels that hold only a few small fronts each
   chain_end.assign(S.nlevels, 0);
   chain_start_of_end.assign(S.nlevels, -1);
@@ -1413,13 +1433,16 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
     const int nslab = slabptr[lv + 1] - slabptr[lv];
     if (use_lists) {
       const i64 ni = eaptr[lv + 1] - eaptr[lv];
-      if (ni > 0) {
+      const bool direct = ea_direct[lv];
+      const i64 nit = direct ? lvslot[lv + 1] - lvslot[lv] : ni;
+      const EaItem* itp = direct ? nullptr : d_eaitems + eaptr[lv];
+      if (nit > 0) {
         if (ea_wide[lv])
-          k_extend_add_list<32><<<(unsigned)((ni * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
-              D, A, d_eaitems + eaptr[lv], ni, L, U);
+          k_extend_add_list<32><<<(unsigned)((nit * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+              D, A, itp, lvslot[lv], nit, L, U);
         else
-          k_extend_add_list<4><<<(unsigned)((ni * 4 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
-              D, A, d_eaitems + eaptr[lv], ni, L, U);
+          k_extend_add_list<4><<<(unsigned)((nit * 4 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+              D, A, itp, lvslot[lv], nit, L, U);
       }
     } else if (nslab > 0) {
       k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);

@@ -102,6 +102,7 @@ struct LinSys {
   std::vector<i64> lvslot, eaptr;   // per level: slot range, extend-add item range
   std::vector<int> lv_tpr;          // per level: lanes per slot in the forward-solve gather
   std::vector<char> ea_wide;        // per level: 32 lanes per extend-add item (else 4)
+  std::vector<char> ea_direct;      // per level: no item list, item w = column slot lvslot[lv] + w
   bool use_lists = true;
   bool use_cluster = true;  // cluster-of-CTAs triangular solves for levels with at most 16 large fronts
   std::vector<void*> owned;
