@@ -217,13 +217,21 @@ __global__ void __launch_bounds__(LDL_THREADS)
   }
 }
 
-// Leaf fronts with one pivot column and at most 33 rows (the private x columns
-// of a cone block: millions of them): one warp per front.
+// Leaf fronts with one pivot column and at most 33 rows (the private x columns of a cone block: millions of them):
+// G lanes per front, G = smallest power of two >= the widest leaf's update rows (4 at C4: three sample rows and
+// the cone row, so a warp handles eight leaves).
+template <int G>
+__device__ __forceinline__ unsigned leaf_mask() {
+  return G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (threadIdx.x & 31 & ~(G - 1)));
+}
+
+template <int G>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_leaf_factor(DevSym S, const int* list, int count, double* L, double* U, double* Dg, const double* reg,
                   double dyn_eps, double* scalars) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / G, lane = threadIdx.x & (G - 1);
   if (w >= count) return;
+  const unsigned mask = leaf_mask<G>();
   const int s = list[w];
   const int c0 = S.col0[s];
   const int nr = (int)(S.rowptr[s + 1] - S.rowptr[s]), nu = nr - 1;
@@ -242,14 +250,15 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const double l = a / d;
   if (lane < nu) Lp[1 + lane] = l;
   for (int j = 0; j < nu; ++j) {
-    const double lj = __shfl_sync(0xffffffffu, l, j);
+    const double lj = __shfl_sync(mask, l, j, G);
     if (lane >= j && lane < nu) Up[lane + (i64)j * nu] -= a * lj;
   }
 }
 
+template <int G>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_leaf_fwd(DevSym S, const int* list, int count, const double* L, const double* xw, double* B) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / G, lane = threadIdx.x & (G - 1);
   if (w >= count) return;
   const int s = list[w];
   const int nu = (int)(S.rowptr[s + 1] - S.rowptr[s]) - 1;
@@ -257,18 +266,28 @@ __global__ void __launch_bounds__(LDL_THREADS)
   if (lane < nu) B[S.Boff[s] + lane] = -(L[S.Loff[s] + 1 + lane] * x1);
 }
 
+template <int G>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_leaf_bwd(DevSym S, const int* list, int count, const double* L, double* xw) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / G, lane = threadIdx.x & (G - 1);
   if (w >= count) return;
+  const unsigned mask = leaf_mask<G>();
   const int s = list[w];
   const i64 rp = S.rowptr[s];
   const int nu = (int)(S.rowptr[s + 1] - rp) - 1;
   double acc = (lane < nu) ? L[S.Loff[s] + 1 + lane] * xw[S.rowidx[rp + 1 + lane]] : 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o);
   if (lane == 0) xw[S.col0[s]] -= acc;
 }
+
+#define QS_LEAF_DISPATCH(kern, grid, ...)                                                 \
+  switch (leaf_group) {                                                                   \
+    case 4: kern<4><<<grid(4), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;                 \
+    case 8: kern<8><<<grid(8), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;                 \
+    case 16: kern<16><<<grid(16), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;              \
+    default: kern<32><<<grid(32), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;              \
+  }
 
 // One CTA per front of the level (children already assembled by k_extend_add):
 // factor the pivot panel, form this front's own update matrix.
@@ -802,7 +821,6 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const int nr = (int)(S.rowptr[s + 1] - rp);
   const double* Lp = L + S.Loff[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gt = rank * LDL_THREADS + tid, gstride = QS_CL * LDL_THREADS;
   __shared__ double part[LDL_THREADS / 32];  // this CTA's partial sums (one per warp), read by rank 0 through DSMEM
   const int last_kb = ((ns - 1) / NB) * NB;
   // Column-oriented products: the 8 x QS_CL = 64 warps of the cluster take the 32 columns of the block, two warps
@@ -1085,6 +1103,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   // work lists: simple leaves (warp per front), general fronts per level (CTA per front),
   // extend-add slabs per level (8 front columns per CTA; only fronts that have children)
   std::vector<int> leaf, gen, small, blk;
+  int leaf_max_nu = 0;
   std::vector<SlabItem> slabs;
   smallptr.assign(S.nlevels + 1, 0);
   blkptr.assign(S.nlevels + 1, 0);
@@ -1101,6 +1120,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
       const bool has_children = S.childptr[s + 1] > S.childptr[s];
       if (!has_children && ns == 1 && nr <= 33) {
         leaf.push_back(s);
+        leaf_max_nu = std::max(leaf_max_nu, nr - 1);
         continue;
       }
       gen.push_back(s);
@@ -1121,6 +1141,8 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
     slabptr[lv + 1] = (int)slabs.size();
   }
   n_leaf = (int)leaf.size();
+  leaf_group = 4;
+  while (leaf_group < 32 && leaf_group < leaf_max_nu) leaf_group <<= 1;
   d_leaf = upload(leaf, &owned, &device_bytes, st);
   d_gen = upload(gen, &owned, &device_bytes, st);
   d_small = upload(small, &owned, &device_bytes, st);
@@ -1420,9 +1442,8 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
   if (S.Uoff[S.nsup] > 0) cudaMemsetAsync(U, 0, S.Uoff[S.nsup] * 8, st);
   k_scatter_values<<<grid_for(knnz), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
   k_add_reg<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D, reg, L);
-  if (n_leaf > 0)
-    k_leaf_factor<<<(unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
-        D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars);
+  auto leaf_grid = [&](int g) { return (unsigned)(((i64)n_leaf * g + LDL_THREADS - 1) / LDL_THREADS); };
+  if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_factor, leaf_grid, D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars)
   for (int lv = 0; lv < S.nlevels; ++lv) {
     if (chain_end[lv] > lv + 1) {  // a run of narrow levels: one single-CTA launch
       const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
@@ -1490,8 +1511,8 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
 
 void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st) {
   k_permute_in<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, d_rhs, xw);
-  const unsigned leaf_grid = (unsigned)(((i64)n_leaf * 32 + LDL_THREADS - 1) / LDL_THREADS);
-  if (n_leaf > 0) k_leaf_fwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw, B);
+  auto leaf_grid = [&](int g) { return (unsigned)(((i64)n_leaf * g + LDL_THREADS - 1) / LDL_THREADS); };
+  if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_fwd, leaf_grid, D, d_leaf, n_leaf, L, xw, B)
   for (int lv = 0; lv < S.nlevels; ++lv) {
     if (chain_end[lv] > lv + 1) {
       const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
@@ -1564,7 +1585,7 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
     const int cnt = smallptr[lv + 1] - smallptr[lv];
     if (cnt > 0) k_solve_bwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw);
   }
-  if (n_leaf > 0) k_leaf_bwd<<<leaf_grid, LDL_THREADS, 0, st>>>(D, d_leaf, n_leaf, L, xw);
+  if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_bwd, leaf_grid, D, d_leaf, n_leaf, L, xw)
   k_permute_out<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, xw, d_sol);
 }
 

@@ -87,6 +87,7 @@ struct LinSys {
   int* d_levelsup = nullptr;
   // work lists built at analysis (see ldl.cu)
   int n_leaf = 0;
+  int leaf_group = 32;  // lanes per leaf front (4, 8, 16 or 32)
   int* d_leaf = nullptr;
   int* d_gen = nullptr;
   SlabItem* d_slabs = nullptr;
