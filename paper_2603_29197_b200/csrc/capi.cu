@@ -3,16 +3,86 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/qsocp_cuda.h"
 #include "cone_kernels.h"
+#include "devmem.h"
 #include "host_setup.h"
 #include "kkt_kernels.h"
 #include "ldl.h"
 #include "ruiz_kernels.h"
 #include "spmv_kernels.h"
+
+// ------------------------------------------------------------ device memory (devmem.h)
+namespace {
+struct DevMem {
+  std::mutex mu;
+  bool ready[64] = {false};
+  bool pooled[64] = {false};
+  cudaStream_t stream[64] = {nullptr};
+  std::unordered_set<void*> from_pool;  // pointers handed out by cudaMallocAsync
+};
+DevMem g_devmem;
+}  // namespace
+
+cudaError_t qs_dev_malloc(void** p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaMalloc(p, bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_devmem.mu);
+    if (!g_devmem.ready[dev]) {
+      g_devmem.ready[dev] = true;
+      int supported = 0;
+      cudaDeviceGetAttribute(&supported, cudaDevAttrMemoryPoolsSupported, dev);
+      cudaMemPool_t pool = nullptr;
+      if (supported && !getenv("QS_NO_MEMPOOL") && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+          cudaStreamCreateWithFlags(&g_devmem.stream[dev], cudaStreamNonBlocking) == cudaSuccess) {
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_devmem.pooled[dev] = true;
+      }
+      cudaGetLastError();
+    }
+  }
+  if (!g_devmem.pooled[dev]) return cudaMalloc(p, bytes);
+  cudaError_t e = cudaMallocAsync(p, bytes, g_devmem.stream[dev]);
+  if (e != cudaSuccess) {  // pool exhausted or fragmented: hand the cached blocks back to the driver and retry once
+    cudaGetLastError();
+    cudaMemPool_t pool = nullptr;
+    cudaStreamSynchronize(g_devmem.stream[dev]);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes, g_devmem.stream[dev]);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cudaMalloc(p, bytes);
+    }
+  }
+  cudaStreamSynchronize(g_devmem.stream[dev]);  // the block may now be used on any stream
+  std::lock_guard<std::mutex> lk(g_devmem.mu);
+  g_devmem.from_pool.insert(*p);
+  return cudaSuccess;
+}
+
+void qs_dev_free(void* p) {
+  if (!p) return;
+  bool pooled = false;
+  {
+    std::lock_guard<std::mutex> lk(g_devmem.mu);
+    pooled = g_devmem.from_pool.erase(p) > 0;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (pooled && dev >= 0 && dev < 64 && g_devmem.stream[dev])
+    cudaFreeAsync(p, g_devmem.stream[dev]);
+  else
+    cudaFree(p);
+}
+
 
 namespace {
 
@@ -28,7 +98,7 @@ struct DevPool {
   T* alloc(size_t count) {
     void* p = nullptr;
     const size_t sz = std::max<size_t>(count, 1) * sizeof(T);
-    if (cudaMalloc(&p, sz) != cudaSuccess) {
+    if (qs_dev_malloc(&p, sz) != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
@@ -44,7 +114,7 @@ struct DevPool {
     return d;
   }
   void release() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) qs_dev_free(p);
     ptrs.clear();
     bytes = 0;
   }

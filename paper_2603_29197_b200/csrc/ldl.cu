@@ -1,6 +1,8 @@
 // GPU supernodal multifrontal LDL' (see ldl.h).
 #include "ldl.h"
 
+#include "devmem.h"
+
 #include <cooperative_groups.h>
 
 #include <chrono>
@@ -1052,7 +1054,7 @@ T* upload(const std::vector<T>& v, std::vector<void*>* owned, size_t* bytes, cud
   g_upload_bytes += v.size() * sizeof(T);
   T* d = nullptr;
   const size_t sz = std::max<size_t>(v.size(), 1) * sizeof(T);
-  if (cudaMalloc(&d, sz) != cudaSuccess) return nullptr;
+  if (qs_dev_malloc((void**)&d, sz) != cudaSuccess) return nullptr;
   if (!v.empty()) cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st);
   owned->push_back(d);
   *bytes += sz;
@@ -1178,7 +1180,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
     if (!d_tiles) return "cudaMalloc failed for the Schur tile list";
     cudaStreamSynchronize(st);
   }
-  if (cudaMalloc((void**)&partial, std::max<i64>(pmax, 1) * 8) != cudaSuccess) return "cudaMalloc failed (solve partials)";
+  if (qs_dev_malloc((void**)&partial, std::max<i64>(pmax, 1) * 8) != cudaSuccess) return "cudaMalloc failed (solve partials)";
   owned.push_back(partial);
   device_bytes += pmax * 8;
   d_slabs = upload(slabs, &owned, &device_bytes, st);
@@ -1370,7 +1372,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   for (i64 k = 0; k < N; ++k) regh[k] = (S.perm[k] < n_pos) ? static_reg : -static_reg;  // kkt.py:48-52
   reg = upload(regh, &owned, &device_bytes, st);
   auto alloc = [&](void** p, size_t bytes) {
-    if (cudaMalloc(p, std::max<size_t>(bytes, 8)) != cudaSuccess) return false;
+    if (qs_dev_malloc(p, std::max<size_t>(bytes, 8)) != cudaSuccess) return false;
     owned.push_back(*p);
     device_bytes += bytes;
     return true;
@@ -1631,7 +1633,7 @@ void LinSys::release() {
   for (GraphEntry& e : solve_graphs) cudaGraphExecDestroy(e.exec);
   factor_graphs.clear();
   solve_graphs.clear();
-  for (void* p : owned) cudaFree(p);
+  for (void* p : owned) qs_dev_free(p);
   owned.clear();
   L = U = Dg = B = xw = reg = nullptr;
   amap = nullptr;
