@@ -246,14 +246,39 @@ int check_launch(qs_handle* h, const char* what) {
   return QS_OK;
 }
 
+// Pinned host mirrors of the scalar block are recycled across handles: cudaMallocHost / cudaFreeHost synchronise the
+// device and showed up as 10-230 ms of handle teardown.
+std::mutex g_pinned_mu;
+std::vector<double*> g_pinned_free;
+
+double* pinned_scalars_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      double* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  double* p = nullptr;
+  if (cudaMallocHost((void**)&p, SC_COUNT * sizeof(double)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void pinned_scalars_put(double* p) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
 bool ensure_scratch(qs_handle* h) {
   if (h->scalars) return true;
-  if (cudaMalloc((void**)&h->scalars, SC_COUNT * sizeof(double)) != cudaSuccess) return false;
+  if (qs_dev_malloc((void**)&h->scalars, SC_COUNT * sizeof(double)) != cudaSuccess) return false;
   cudaMemsetAsync(h->scalars, 0, SC_COUNT * sizeof(double), h->stream);
-  if (cudaMallocHost((void**)&h->scalars_host, SC_COUNT * sizeof(double)) != cudaSuccess) return false;
-  if (cudaMalloc((void**)&h->gr.partial, (size_t)QS_MAX_GRID * QS_RED_MAXK * sizeof(double)) != cudaSuccess)
+  h->scalars_host = pinned_scalars_get();
+  if (!h->scalars_host) return false;
+  if (qs_dev_malloc((void**)&h->gr.partial, (size_t)QS_MAX_GRID * QS_RED_MAXK * sizeof(double)) != cudaSuccess)
     return false;
-  if (cudaMalloc((void**)&h->gr.counter, sizeof(unsigned)) != cudaSuccess) return false;
+  if (qs_dev_malloc((void**)&h->gr.counter, sizeof(unsigned)) != cudaSuccess) return false;
   cudaMemsetAsync(h->gr.counter, 0, sizeof(unsigned), h->stream);
   return true;
 }
@@ -453,16 +478,30 @@ void qs_destroy(qs_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
+  const bool verbose = getenv("QS_VERBOSE") != nullptr;
+  auto t_mark = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (verbose) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[qs destroy] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t_mark).count());
+      t_mark = now;
+    }
+  };
   h->tm.release();
+  lap("timers");
   h->ls.release();
+  lap("LDL' (graphs + storage)");
   h->cone_pool.release();
   h->prob_pool.release();
-  if (h->scalars) cudaFree(h->scalars);
-  if (h->scalars_host) cudaFreeHost(h->scalars_host);
-  if (h->gr.partial) cudaFree(h->gr.partial);
-  if (h->gr.counter) cudaFree(h->gr.counter);
+  lap("problem + cone pools");
+  if (h->scalars) qs_dev_free(h->scalars);
+  if (h->scalars_host) pinned_scalars_put(h->scalars_host);
+  if (h->gr.partial) qs_dev_free(h->gr.partial);
+  if (h->gr.counter) qs_dev_free(h->gr.counter);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  lap("scratch + stream");
   delete h;
+  lap("host vectors");
 }
 
 const char* qs_last_error(qs_handle* h) { return h ? h->err.c_str() : g_error.c_str(); }
