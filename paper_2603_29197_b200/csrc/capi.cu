@@ -857,8 +857,23 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   const i64 nnzA = Ap[n], nnzG = Gp[n], nnzP = Pp[n];
   std::vector<i64> Arp(p + 1), Ari(nnzA), Grp(m + 1), Gri(nnzG);
   std::vector<double> Arx(nnzA), Grx(nnzG);
-  hs_transpose(p, n, (const i64*)Ap, (const i64*)Ai, Ax, Arp.data(), Ari.data(), Arx.data());
-  hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, Gx, Grp.data(), Gri.data(), Grx.data());
+  // one transpose per matrix: the INDEX vector goes through it (where does every entry of the row view come from --
+  // kept for value-only updates), the values follow by a gather
+  std::vector<int> ar_map(nnzA), gr_map(nnzG);
+  {
+    std::vector<double> iota(std::max(nnzA, nnzG));
+    for (size_t k = 0; k < iota.size(); ++k) iota[k] = (double)k;
+    hs_transpose(p, n, (const i64*)Ap, (const i64*)Ai, iota.data(), Arp.data(), Ari.data(), Arx.data());
+    for (i64 k = 0; k < nnzA; ++k) {
+      ar_map[k] = (int)Arx[k];
+      Arx[k] = Ax[ar_map[k]];
+    }
+    hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, iota.data(), Grp.data(), Gri.data(), Grx.data());
+    for (i64 k = 0; k < nnzG; ++k) {
+      gr_map[k] = (int)Grx[k];
+      Grx[k] = Gx[gr_map[k]];
+    }
+  }
   // Pf = P + P' - diag(P), rows ascending
   std::vector<i64> Pfp(n + 1, 0);
   for (i64 j = 0; j < n; ++j)
@@ -889,17 +904,6 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
         Pfx[next[i]++] = Px[k];
       }
     }
-  }
-  // where every entry of the row views of A and G comes from (for value-only updates): transpose the index vector
-  std::vector<int> ar_map(nnzA), gr_map(nnzG);
-  {
-    std::vector<double> iota(std::max(nnzA, nnzG)), tmp(std::max(nnzA, nnzG));
-    for (size_t k = 0; k < iota.size(); ++k) iota[k] = (double)k;
-    std::vector<i64> tp(std::max(p, m) + 1), ti(std::max(nnzA, nnzG));
-    hs_transpose(p, n, (const i64*)Ap, (const i64*)Ai, iota.data(), tp.data(), ti.data(), tmp.data());
-    for (i64 k = 0; k < nnzA; ++k) ar_map[k] = (int)tmp[k];
-    hs_transpose(m, n, (const i64*)Gp, (const i64*)Gi, iota.data(), tp.data(), ti.data(), tmp.data());
-    for (i64 k = 0; k < nnzG; ++k) gr_map[k] = (int)tmp[k];
   }
   lap("row views + value maps (host)");
   h->nnzP = nnzP;
