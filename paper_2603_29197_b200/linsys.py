@@ -22,31 +22,38 @@ from .sparse import SparseMatrixCSC, csc_from_triplets, empty_csc
 
 
 class LinsysBackend(ABC):
+    """The plugin contract a linear-system backend fulfils (reference: linsys.py:24-51).
+
+    Lifecycle: ``initialize`` exactly once, then any number of ``update`` -> ``factor`` -> ``solve`` rounds, then
+    ``close``.  ``n_factor`` / ``n_solve`` count completed factorisations and refined solves (the IPM driver relies on
+    factors = iterations + 1 and solves = 2 iterations + 2).
+    """
+
     name = "abstract"
 
     def __init__(self):
-        self.n_factor = 0
-        self.n_solve = 0
         self._initialized = False
+        self.n_factor = 0  # completed numeric factorisations
+        self.n_solve = 0   # completed refined solves
 
     @abstractmethod
     def initialize(self, kkt, settings: Settings, ordering: str = "amd") -> None:
-        """One-time analysis of the KKT pattern. Must be called exactly once."""
-
-    @abstractmethod
-    def factor(self) -> None:
-        """Numeric refactorization of the current KKT values."""
-
-    @abstractmethod
-    def solve(self, rhs: np.ndarray) -> np.ndarray:
-        """Triangular solves plus iterative refinement for one right-hand side."""
+        """Analyse the KKT pattern (ordering + symbolic factorisation).  A second call is a RuntimeError."""
 
     @abstractmethod
     def update(self, scaling: NTScalingSet) -> None:
-        """Scatter fresh -W^T W values into the KKT matrix."""
+        """Write the -W'W block of the given Nesterov-Todd scaling into the KKT values."""
+
+    @abstractmethod
+    def factor(self) -> None:
+        """Refactorise the KKT matrix numerically with its current values."""
+
+    @abstractmethod
+    def solve(self, rhs: np.ndarray) -> np.ndarray:
+        """K x = rhs by the current factor, with iterative refinement against the unregularised K."""
 
     def close(self) -> None:
-        pass
+        """Release whatever the backend holds; the default holds nothing."""
 
 
 def _problem_from_kkt(kkt) -> ProblemData:
