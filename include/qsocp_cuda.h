@@ -80,6 +80,10 @@ const char* qs_last_error(qs_handle* h);
 /* run the handle's work on an existing stream (e.g. torch's current stream) */
 int qs_set_stream(qs_handle* h, void* cuda_stream);
 int qs_sync(qs_handle* h);
+/* page-lock / release caller-owned host memory (a mapped problem file, fileio.py of this package; the reference
+ * reads its text format into fresh arrays, fileio.py:120-122) so that qs_setup's copies are not staged */
+int qs_host_register(const void* ptr, int64_t bytes);
+int qs_host_unregister(const void* ptr);
 
 /* ---- host-side structure (no GPU needed) ---------------------------------
  * assemble_kkt (kkt.py:55-135): pattern, values with the scaling block at -I,

@@ -205,6 +205,7 @@ def gen_problems():
         kkt2 = rkkt.assemble_kkt(d)
         be = make_backend("builtin")
         be.initialize(kkt2, Settings())
+        g["amd_perm"] = np.asarray(be.symbolic.perm.forward, dtype=np.int64)  # _amd.py via sparse.py:205-222
         it0 = ripm.initialize_iterate(d, kkt2, be)
         r0 = ripm.compute_residuals(d, it0)
         g["res0_r_dual"], g["res0_r_eq"], g["res0_r_cone"] = r0.r_dual, r0.r_eq, r0.r_cone
@@ -220,8 +221,18 @@ def gen_problems():
         f.write("\n".join(names) + "\n")
 
 
+def gen_problem_file():
+    """A QOCOPROB 1 text file written by the reference's own save_problem (fileio.py:62-64): the reader of
+    paper_2603_29197_b200/fileio.py must load it to the same arrays, and its writer must produce the same text."""
+    from qsocp.fileio import save_problem
+
+    d = dict(small_problems())["portfolio_4"]
+    save_problem(d, os.path.join(OUT, "portfolio_4.qocoprob"))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     gen_cones()
     gen_problems()
+    gen_problem_file()
     print("reference version", qsocp.__version__)

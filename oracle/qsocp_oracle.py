@@ -12,12 +12,13 @@ Parity status: PINNED -- see tests/test_oracle_pinned.py (direct comparison
 with the imported reference when /root/reference exists) and tests/golden/
 (fixtures produced by the reference through oracle/gen_golden.py).
 
-The only deliberate difference: the fill-reducing ordering.  The reference's
-AMD (`_amd.py`) is out of the hot-path scope; the
-oracle takes the permutation as an argument (``perm=``), defaults to the
-ordering routine of the product's host library when that is built (ordering
-changes fill and rounding only, never the algorithm) and otherwise to the
-natural order.
+The oracle is self-contained: it never imports the product package nor loads
+libqsocp_cuda.so.  The fill-reducing ordering is the reference's own AMD
+(`_amd.py`), restated in ``qsocp_oracle_amd.c`` and pinned element by element
+against the reference's permutation, so ``solve(data)`` with no arguments is
+the reference's ``solve(data)`` bit for bit.  A permutation can still be
+handed in (``perm=``) -- e.g. an ordering computed elsewhere and stored in a
+problem file -- which changes fill and rounding only, never the algorithm.
 """
 
 from __future__ import annotations
@@ -43,11 +44,14 @@ _i64 = np.int64
 _f64 = np.float64
 
 
+_SRC = ("qsocp_oracle.c", "qsocp_oracle_amd.c")
+
+
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "qsocp_oracle.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, f) for f in _SRC]
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(f) for f in srcs):
         subprocess.check_call(
-            ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _SO, src, "-lm"]
+            ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _SO, *srcs, "-lm"]
         )
     return _SO
 
@@ -62,6 +66,7 @@ def lib():
         L.orc_soc_max_step.restype = ctypes.c_double
         L.orc_soc_violation.restype = ctypes.c_double
         L.orc_ldl_factor.restype = ctypes.c_int64
+        L.orc_amd_kernel.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -365,21 +370,46 @@ def write_scaling(kkt: KKT, sc: Scaling) -> None:  # kkt.py:146-150
 
 
 # -------------------------------------------------------------------- ldl ----
-def default_perm(K, kkt=None, cone=None) -> np.ndarray:
-    """Fill-reducing order.  See the module docstring for why this is not the
-    reference's `_amd.py`.  When the cone layout is known the SOC blocks are
-    handed over as cliques, so the CPU baseline factorises with the same
-    (best available) ordering as the GPU path."""
-    try:
-        from paper_2603_29197_b200 import ordering as _ord
+def amd_order(n, col_ptr, row_idx, heap_words=None) -> np.ndarray:  # _amd.py:393-419
+    """AMD permutation of a symmetric pattern given by its upper triangle: builds
+    A + A' without the diagonal (rows of every column in the order the reference's
+    stable argsort leaves them) and runs the C restatement of `_amd_kernel`."""
+    if n == 0:
+        return np.empty(0, dtype=_i64)
+    col_ptr = np.asarray(col_ptr, dtype=_i64)
+    cols = np.repeat(np.arange(n, dtype=_i64), np.diff(col_ptr))
+    rows = np.asarray(row_idx, dtype=_i64)
+    off = rows != cols
+    rows, cols = rows[off], cols[off]
+    counts = np.bincount(rows, minlength=n) + np.bincount(cols, minlength=n)
+    cnz = int(counts.sum())
+    nzmax = cnz + cnz // 5 + 8 * n + 16
+    Cp = np.zeros(n + 2, dtype=_i64)
+    np.cumsum(counts, out=Cp[1:n + 1])
+    Ci = np.empty(nzmax, dtype=_i64)
+    rr = np.concatenate([rows, cols])
+    cc = np.concatenate([cols, rows])
+    del rows, cols
+    Ci[:cnz] = rr[np.argsort(cc, kind="stable")]
+    del rr, cc
+    # the reference's heap has 4*cnz+4n+64 words; the pivot sequence does not depend on the capacity
+    # (a full heap is compacted to its live keys), so very large patterns may use less memory
+    cap = max(4 * cnz + 4 * n + 64, 1024) if heap_words is None else max(int(heap_words), 2 * n + 64)
+    heap = np.empty(cap, dtype=_i64)
+    seen = np.zeros(n + 1, dtype=_i64)
+    order = np.empty(n, dtype=_i64)
+    got = lib().orc_amd_kernel(_c64(n), _p(Cp), _p(Ci), _c64(nzmax), _c64(cnz), _p(heap), _c64(cap),
+                               _p(seen), _p(order))
+    if got != n:
+        raise RuntimeError("ordering failed to converge")
+    return order
 
-        if kkt is not None and cone is not None and len(cone.soc_dims):
-            starts, dims = soc_layout(cone)
-            return _ord.analyze(K.cols, K.col_pointers, K.row_indices, "amd", None,
-                                starts + kkt.n + kkt.p, dims)[0]
-        return _ord.amd_order_upper(K.cols, K.col_pointers, K.row_indices)
-    except Exception:
-        return np.arange(K.cols, dtype=_i64)
+
+def default_perm(K, kkt=None, cone=None) -> np.ndarray:
+    """sparse.py:205-222 (`fill_reducing_order(..., "amd")`): the reference's AMD on the full KKT pattern."""
+    cnz2 = 2 * int(K.col_pointers[-1])
+    return amd_order(K.cols, K.col_pointers, K.row_indices,
+                     heap_words=None if cnz2 < 50_000_000 else cnz2 // 2 + 4 * K.cols + 64)
 
 
 @dataclass

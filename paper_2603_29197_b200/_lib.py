@@ -52,6 +52,8 @@ SIGNATURES = {
     "qs_last_error": (C.c_char_p, [vp]),
     "qs_set_stream": (C.c_int, [vp, vp]),
     "qs_sync": (C.c_int, [vp]),
+    "qs_host_register": (C.c_int, [vp, C.c_int64]),
+    "qs_host_unregister": (C.c_int, [vp]),
     "qs_kkt_nnz": (C.c_int64, [C.c_int64] * 5 + [vp, vp, vp, C.c_int64, C.c_int64]),
     "qs_kkt_slot_count": (C.c_int64, [C.c_int64, C.c_int64, vp]),
     "qs_kkt_assemble": (C.c_int, [C.c_int64] * 5 + [vp] * 16),

@@ -216,6 +216,7 @@ struct qs_handle {
   i64 n_factor = 0, n_solve = 0;
   // ---- state
   double *x = nullptr, *y = nullptr, *z = nullptr, *s = nullptr;
+  double *x2 = nullptr, *y2 = nullptr, *z2 = nullptr, *s2 = nullptr;  // next iterate; swapped in when the step is good
   double *w = nullptr, *eta = nullptr, *wbar = nullptr, *lam = nullptr, *lam_sq = nullptr;
   double *d = nullptr, *dcomp = nullptr, *wdz = nullptr, *ds = nullptr, *r_cone = nullptr, *w2vz = nullptr;
   double *rhs = nullptr, *sol = nullptr, *xa = nullptr, *xb = nullptr, *ra = nullptr, *rb = nullptr, *dx = nullptr;
@@ -512,6 +513,31 @@ int qs_set_stream(qs_handle* h, void* cuda_stream) {
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   h->stream = (cudaStream_t)cuda_stream;
   h->own_stream = false;
+  return QS_OK;
+}
+
+// Page-lock caller memory (e.g. a mapped problem file) so host -> device copies skip the driver's staging buffer.
+int qs_host_register(const void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return QS_E_INVALID;
+  cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), (size_t)bytes, cudaHostRegisterReadOnly | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    e = cudaHostRegister(const_cast<void*>(ptr), (size_t)bytes, cudaHostRegisterPortable);
+  }
+  if (e != cudaSuccess) {
+    g_error = std::string("cudaHostRegister: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return QS_E_CUDA;
+  }
+  return QS_OK;
+}
+
+int qs_host_unregister(const void* ptr) {
+  if (!ptr) return QS_E_INVALID;
+  if (cudaHostUnregister(const_cast<void*>(ptr)) != cudaSuccess) {
+    cudaGetLastError();
+    return QS_E_CUDA;
+  }
   return QS_OK;
 }
 
@@ -1029,6 +1055,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   h->field = P.alloc<double>(count);         \
   if (!h->field) return fail(h, QS_E_MEMORY, "out of device memory for the iterate");
   ALLOC(x, n) ALLOC(y, p) ALLOC(z, m) ALLOC(s, m)
+  ALLOC(x2, n) ALLOC(y2, p) ALLOC(z2, m) ALLOC(s2, m)
   ALLOC(w, l) ALLOC(eta, nsoc) ALLOC(wbar, m) ALLOC(lam, m) ALLOC(lam_sq, m)
   ALLOC(d, m) ALLOC(dcomp, m) ALLOC(wdz, m) ALLOC(ds, m) ALLOC(r_cone, m) ALLOC(w2vz, m) ALLOC(tmp_m, m)
   ALLOC(rhs, N) ALLOC(xa, N) ALLOC(xb, N) ALLOC(ra, N) ALLOC(rb, N) ALLOC(dx, N)
@@ -1294,7 +1321,8 @@ int qs_step(qs_handle* h, qs_step_info* out) {
   h->tm.begin(T_CONE, st);
   qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, nullptr, h->ds, h->scalars, 1,
                  h->st.step_fraction, h->gr, st);
-  qsk_update_iterate((int)n, (int)p, (int)m, h->x, h->y, h->z, h->s, h->sol, h->ds, h->deg, h->scalars, h->gr, st);
+  qsk_update_iterate((int)n, (int)p, (int)m, h->x, h->y, h->z, h->s, h->x2, h->y2, h->z2, h->s2, h->sol, h->ds, h->deg,
+                     h->scalars, h->gr, st);
   h->tm.end(st);
   h->launches += 8;
   rc = check_launch(h, "ipm_step");
@@ -1302,6 +1330,14 @@ int qs_step(qs_handle* h, qs_step_info* out) {
   rc = fetch_scalars(h);
   if (rc) return rc;
   const double* sc = h->scalars_host;
+  // the new iterate replaces the old one only when the step raised nothing (the reference assigns `it = nxt` after
+  // ipm_step returned, ipm.py:219-235,286): a NumericalError result carries the last good iterate
+  if (flags_of(sc) == 0) {
+    std::swap(h->x, h->x2);
+    std::swap(h->y, h->y2);
+    std::swap(h->z, h->z2);
+    std::swap(h->s, h->s2);
+  }
   if (out) {
     out->alpha = sc[SC_ALPHA];
     out->alpha_affine = sc[SC_ALPHA_AFF];

@@ -825,35 +825,45 @@ __global__ void __launch_bounds__(QS_THREADS) k_mu_aff(int m, const double* s, c
   });
 }
 
-__global__ void __launch_bounds__(QS_THREADS) k_update_iterate(int n, int p, int m, double* x, double* y, double* z,
-                                                               double* s, const double* sol, const double* ds,
-                                                               double deg, double* scalars, GridRed gr) {
-  // it' = it + alpha (dx, dy, dz, ds); mu' = s'.z' / deg; finite check (ipm.py:220-234)
+__global__ void __launch_bounds__(QS_THREADS) k_update_iterate(int n, int p, int m, const double* x, const double* y,
+                                                               const double* z, const double* s, double* xo, double* yo,
+                                                               double* zo, double* so, const double* sol,
+                                                               const double* ds, double deg, double* scalars, GridRed gr) {
+  // it' = it + alpha (dx, dy, dz, ds); mu' = s'.z' / deg; finite check (ipm.py:220-234).  The new iterate goes to
+  // (xo, yo, zo, so): the reference builds `nxt` and raises before it replaces `it` (ipm.py:219-229), so a failed
+  // step must leave the last good iterate intact -- the host swaps the buffers only when no flag is raised.
   const double a = scalars[SC_ALPHA];
+  const bool bad_step = scalars[SC_FLAG_BAD_STEP] != 0.0;  // alpha <= 0 or non-finite: nothing to apply
   double v[2] = {0.0, 0.0};
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-  for (int i = tid; i < n; i += nth) {
-    const double t = x[i] + a * sol[i];
-    x[i] = t;
-    if (!qs_finite(t)) v[1] = 1.0;
-  }
-  for (int i = tid; i < p; i += nth) {
-    const double t = y[i] + a * sol[n + i];
-    y[i] = t;
-    if (!qs_finite(t)) v[1] = 1.0;
-  }
-  for (int i = tid; i < m; i += nth) {
-    const double zt = z[i] + a * sol[n + p + i];
-    const double st = s[i] + a * ds[i];
-    z[i] = zt;
-    s[i] = st;
-    v[0] += st * zt;
-    if (!qs_finite(zt) || !qs_finite(st)) v[1] = 1.0;
+  if (!bad_step) {
+    for (int i = tid; i < n; i += nth) {
+      const double t = x[i] + a * sol[i];
+      xo[i] = t;
+      if (!qs_finite(t)) v[1] = 1.0;
+    }
+    for (int i = tid; i < p; i += nth) {
+      const double t = y[i] + a * sol[n + i];
+      yo[i] = t;
+      if (!qs_finite(t)) v[1] = 1.0;
+    }
+    for (int i = tid; i < m; i += nth) {
+      const double zt = z[i] + a * sol[n + p + i];
+      const double st = s[i] + a * ds[i];
+      zo[i] = zt;
+      so[i] = st;
+      v[0] += st * zt;
+      if (!qs_finite(zt) || !qs_finite(st)) v[1] = 1.0;
+    }
   }
   using Ops = RedOps<RED_SUM, RED_MAX>;
   qs_grid_reduce<Ops>(v, gr, [=](double (&t)[2]) {
+    if (bad_step) return;  // SC_MU keeps the value of the iterate that stays
+    if (t[1] != 0.0) {  // only the vectors are tested here (ipm.py:227-229); a non-finite s'.z' of finite
+      scalars[SC_FLAG_NONFINITE] = 1.0;  // vectors surfaces in the next residual phase, as in the reference
+      return;
+    }
     scalars[SC_MU] = t[0] / deg;
-    if (t[1] != 0.0 || !qs_finite(t[0])) scalars[SC_FLAG_NONFINITE] = 1.0;
   });
 }
 
@@ -939,10 +949,11 @@ void qsk_mu_aff(int m, const double* s, const double* z, const double* ds, const
   k_mu_aff<<<vec_grid(m), QS_THREADS, 0, st>>>(m, s, z, ds, dz, deg, scalars, gr);
 }
 
-void qsk_update_iterate(int n, int p, int m, double* x, double* y, double* z, double* s, const double* sol,
-                        const double* ds, double deg, double* scalars, GridRed gr, cudaStream_t st) {
+void qsk_update_iterate(int n, int p, int m, const double* x, const double* y, const double* z, const double* s,
+                        double* xo, double* yo, double* zo, double* so, const double* sol, const double* ds, double deg,
+                        double* scalars, GridRed gr, cudaStream_t st) {
   i64 big = n > m ? n : m;
-  k_update_iterate<<<vec_grid(big), QS_THREADS, 0, st>>>(n, p, m, x, y, z, s, sol, ds, deg, scalars, gr);
+  k_update_iterate<<<vec_grid(big), QS_THREADS, 0, st>>>(n, p, m, x, y, z, s, xo, yo, zo, so, sol, ds, deg, scalars, gr);
 }
 
 void qsk_dot(int m, const double* a, const double* b, double scale, double* out, GridRed gr, cudaStream_t st) {

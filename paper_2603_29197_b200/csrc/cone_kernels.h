@@ -24,6 +24,7 @@ void qsk_post_solve(const ConeLayout& L, const double* w, const double* eta, con
                     int corrector, double step_fraction, GridRed gr, cudaStream_t st);
 void qsk_mu_aff(int m, const double* s, const double* z, const double* ds, const double* dz, double deg,
                 double* scalars, GridRed gr, cudaStream_t st);
-void qsk_update_iterate(int n, int p, int m, double* x, double* y, double* z, double* s, const double* sol,
-                        const double* ds, double deg, double* scalars, GridRed gr, cudaStream_t st);
+void qsk_update_iterate(int n, int p, int m, const double* x, const double* y, const double* z, const double* s,
+                        double* xo, double* yo, double* zo, double* so, const double* sol, const double* ds, double deg,
+                        double* scalars, GridRed gr, cudaStream_t st);
 void qsk_dot(int m, const double* a, const double* b, double scale, double* out, GridRed gr, cudaStream_t st);

@@ -83,20 +83,48 @@ def test_kkt_and_spmv_match_reference_golden(oracle, name):
 
 
 @pytest.mark.parametrize("name", golden_problem_names())
+def test_ordering_matches_reference_golden(oracle, name):
+    """The oracle's AMD (oracle/qsocp_oracle_amd.c) returns the reference's permutation element by
+    element, whatever the heap capacity (a full heap is compacted to its live keys)."""
+    g = load_golden(name)
+    K = oracle.assemble_kkt(problem_from_golden(g)).matrix
+    for cap in (None, 8):
+        perm = oracle.amd_order(K.cols, K.col_pointers, K.row_indices, heap_words=cap)
+        assert perm.dtype == np.int64 and np.array_equal(perm, g["amd_perm"])
+
+
+@pytest.mark.parametrize("name", golden_problem_names())
 def test_solve_matches_reference_golden(oracle, name):
-    """End to end.  The oracle's ordering differs from the reference's AMD (out
-    of scope), so iterates agree to rounding, not bitwise: iterations equal,
-    objective / solution to 1e-6 relative (the north-star tolerance)."""
+    """End to end, no argument handed over: same ordering, same factorisation, same arithmetic as the
+    reference, so the result is the reference's bit for bit."""
     g = load_golden(name)
     d = problem_from_golden(g)
-    res = oracle.solve(d)
+    mus = []
+    res = oracle.solve(d, hook=lambda it: mus.append(it.mu))
     assert res.status == str(g["status"])
-    assert abs(res.iterations - int(g["iterations"])) <= 1
-    assert res.factor_count == res.iterations + 1 and res.solve_count == 2 * res.iterations + 2
-    assert abs(res.objective - float(g["objective"])) <= 1e-6 * max(1.0, abs(float(g["objective"])))
+    assert res.iterations == int(g["iterations"])
+    assert res.factor_count == int(g["factor_count"]) and res.solve_count == int(g["solve_count"])
+    assert res.objective == float(g["objective"])
+    assert np.array_equal(np.asarray(mus), g["trace_mu"])
     for k in "xyzs":
-        ref = g[k]
-        assert np.max(np.abs(getattr(res, k) - ref), initial=0.0) <= 1e-5 * max(1.0, np.max(np.abs(ref), initial=0.0))
+        assert np.array_equal(getattr(res, k), g[k]), k
+
+
+def test_oracle_never_touches_the_product_library(oracle):
+    """The checker must be independent of what it checks: solving with the oracle maps neither
+    libqsocp_cuda.so (fresh interpreter; the data classes of the problem come from the package, its
+    native library must stay unloaded)."""
+    import subprocess
+
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "from util import load_golden, problem_from_golden\n"
+            "from oracle import qsocp_oracle as o\n"
+            "r = o.solve(problem_from_golden(load_golden('portfolio_4')))\n"
+            "assert r.status == 'Solved'\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert 'libqsocp_cuda' not in maps, 'oracle mapped the product library'\n"
+            % (os.path.dirname(GOLDEN), os.path.dirname(os.path.dirname(GOLDEN))))
+    subprocess.run([sys.executable, "-c", code], check=True)
 
 
 @pytest.mark.skipif(not HAVE_REF, reason="reference tree not present on this machine")
@@ -132,6 +160,16 @@ def test_direct_against_imported_reference(oracle):
         assert np.array_equal(oracle.jordan_divide(a.lam, v, cone), rc.jordan_divide(b.lam, v, rcone))
         assert oracle.max_step_to_boundary(s, u, cone) == rc.max_step_to_boundary(s, u, rcone)
         assert oracle.interior_violation(u, cone) == rc.interior_violation(u, rcone)
+    # ordering: the reference's amd_order on fresh patterns (random QP, group lasso with dense SOC blocks, MPC chain)
+    from qsocp import _amd
+    from paper_2603_29197_b200 import configs
+
+    for d in (configs.random_qp(n=300, p=60, m=500, density=0.03, seed=3), configs.group_lasso(groups=24, samples=30, seed=1),
+              configs.mpc(horizon=12, seed=5), configs.portfolio(assets=400, factors=8, sector=20, seed=2)):
+        K = oracle.assemble_kkt(d).matrix
+        want = _amd.amd_order(K.cols, K.col_pointers, K.row_indices)
+        assert np.array_equal(oracle.amd_order(K.cols, K.col_pointers, K.row_indices), want)
+        assert np.array_equal(oracle.amd_order(K.cols, K.col_pointers, K.row_indices, heap_words=1), want)
     # the reference's own LDL with the reference's AMD permutation handed to the oracle: bitwise trace
     for name in ("huber_20", "tv_denoising_8", "random_1", "group_lasso_3"):
         g = load_golden(name)
@@ -145,6 +183,8 @@ def test_direct_against_imported_reference(oracle):
         perm = be.symbolic.perm.forward
         res = oracle.solve(d, perm=np.asarray(perm))
         ref = qsocp.solve(rd)
+        own = oracle.solve(d)  # the oracle's own ordering is the same permutation
+        assert own.objective == ref.objective and np.array_equal(own.x, ref.x)
         assert res.iterations == ref.iterations
         assert res.objective == ref.objective
         for k in "xyzs":
