@@ -14,7 +14,7 @@ import numpy as np
 from .errors import CudaUnavailable, DimensionMismatch, NotInterior, NumericalError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqsocp_cuda.so")
+LIB_PATH = os.environ.get("QS_LIB_PATH") or os.path.join(HERE, "libqsocp_cuda.so")  # QS_LIB_PATH: A/B builds
 
 QS_OK, QS_E_INVALID, QS_E_CUDA, QS_E_NOT_INTERIOR, QS_E_NUMERICAL, QS_E_MEMORY, QS_E_DIMENSION = range(7)
 

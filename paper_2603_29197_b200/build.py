@@ -45,6 +45,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         if force or _stale(obj, [src] + hdrs):
             flags = [x for x in NVCC_FLAGS if not (f in FMA_OK and x == "-fmad=false")]
+            if os.environ.get("QS_CONE_VARIANTS") and f == "cone_kernels.cu":  # tuning: slot-count instantiations
+                flags = flags + ["-DQS_CONE_VARIANTS=" + os.environ["QS_CONE_VARIANTS"]]
             jobs.append([NVCC, *flags, "-c", src, "-o", obj])
     for f in CPP:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")

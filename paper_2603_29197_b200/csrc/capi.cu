@@ -1,5 +1,6 @@
 // C ABI of libqsocp_cuda.so (include/qsocp_cuda.h): handle, setup, the
 // per-kernel entry points and the device-resident IPM phases.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -327,10 +328,10 @@ bool make_csr(qs_handle* h, Csr* M, i64 rows, i64 cols, const i64* ptr, const i6
   return M->ptr && M->idx && M->val;
 }
 
-int scatter_scaling(qs_handle* h, const double* w, const double* eta, const double* wbar) {
+int scatter_scaling(qs_handle* h, const double* w, const double* eta, const double* wbar, bool have_consts = false) {
   h->tm.begin(T_KKT, h->stream);
-  qsk_neg_wtw(h->wp, h->direct_ok ? 2 : 1, w, eta, wbar, h->d_pos, h->d_Kx, h->stream);
-  h->launches += 2;
+  qsk_neg_wtw(h->wp, h->direct_ok ? 2 : 1, w, eta, wbar, h->d_pos, h->d_Kx, h->stream, have_consts);
+  h->launches += have_consts ? 1 : 2;
   h->tm.end(h->stream);
   return check_launch(h, "neg_wtw scatter");
 }
@@ -634,7 +635,9 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
     while (G < 32 && G < atoi(e)) G <<= 1;
   }
   if (const char* e = getenv("QS_CONE_SINGLE")) single = atoi(e) != 0;
-  const i64 small_cap = std::min<i64>((i64)G * 8, big_threshold);
+  // register-resident ops need dim <= 8 G; when every op runs chunked (single == 0) a lane group takes any dim
+  i64 small_cap = std::min<i64>(single == 0 ? big_threshold : (i64)G * 8, big_threshold);
+  if (const char* e = getenv("QS_CONE_SMALLCAP")) small_cap = std::max(1, atoi(e));
   for (i64 k = 0; k < nsoc; ++k) {
     m += q[k];
     if (m >= ((i64)1 << 31)) return fail(h, QS_E_DIMENSION, "m exceeds 2^31");
@@ -648,12 +651,19 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   L.l = (int)l;
   L.nsoc = (int)nsoc;
   L.soc_ptr = h->cone_pool.upload(ptr.data(), ptr.size(), h->stream);
+  // small cones sorted by dimension, largest first: the lane groups of a CTA then work on cones of similar size
+  // (no warp waits at the CTA's final barrier for a much longer neighbour, the per-size dispatch does not diverge)
+  // and the shortest cones fill the tail of the persistent grid
+  std::stable_sort(small_ids.begin(), small_ids.end(), [&](int a, int b) { return q[a] > q[b]; });
+  if (getenv("QS_CONE_UNSORTED")) std::sort(small_ids.begin(), small_ids.end());
   L.nsmall = (int)small_ids.size();
   L.nbig = (int)big_ids.size();
-  L.small_ids = big_ids.empty() ? nullptr : h->cone_pool.upload(small_ids.data(), small_ids.size(), h->stream);
+  L.small_ids = small_ids.empty() ? nullptr : h->cone_pool.upload(small_ids.data(), small_ids.size(), h->stream);
   L.big_ids = big_ids.empty() ? nullptr : h->cone_pool.upload(big_ids.data(), big_ids.size(), h->stream);
   L.group = G;
   L.single = single;
+  L.waves = 1;
+  if (const char* e = getenv("QS_CONE_WAVES")) L.waves = std::max(1, atoi(e));
   h->deg = (double)(l + nsoc);
   // -W'W plan: column tiles of ~QS_WTW_TILE block entries
   WtwPlan& P = h->wp;
@@ -723,7 +733,8 @@ int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q, int64_
   P.e2 = h->cone_pool.alloc<double>(nsoc);
   h->cone_tmp = h->cone_pool.alloc<double>(m);
   CK(h, cudaStreamSynchronize(h->stream));
-  if (!L.soc_ptr || !P.cone_of_col || !P.tile_ptr || !P.c4 || !P.e2 || !h->cone_tmp)
+  if (!L.soc_ptr || !P.cone_of_col || !P.tile_ptr || !P.c4 || !P.e2 || !h->cone_tmp ||
+      (!small_ids.empty() && !L.small_ids))
     return fail(h, QS_E_MEMORY, "cone layout alloc");
   h->have_cones = true;
   return QS_OK;
@@ -738,7 +749,8 @@ int qs_nt_scaling(qs_handle* h, const double* s, const double* z, double* w, dou
                   double* lam_sq, int* not_interior_host) {
   NEED_CONES(h)
   if (not_interior_host) cudaMemsetAsync(h->scalars + SC_FLAG_NOT_INTERIOR, 0, sizeof(double), h->stream);
-  qsk_nt_scaling(h->L, s, z, w, eta, wbar, lam, lam_sq, h->scalars, h->stream);
+  qsk_nt_scaling(h->L, s, z, w, eta, wbar, lam, lam_sq, nullptr, nullptr, nullptr, nullptr, nullptr, h->scalars,
+                 h->stream);
   h->launches++;
   int rc = check_launch(h, "nt_scaling");
   if (rc || !not_interior_host) return rc;
@@ -1295,36 +1307,34 @@ int qs_step(qs_handle* h, qs_step_info* out) {
   const ConeLayout& L = h->L;
   const i64 n = h->n, p = h->p, m = h->m;
   clear_flags(h);
+  // scaling, lam o lam, the -W'W constants and the predictor's third RHS block (d_comp = -lam o lam) in one pass
   h->tm.begin(T_CONE, st);
-  qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->scalars, st);
+  qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->wp.c4, h->wp.e2, h->r_cone, h->d,
+                 h->rhs + n + p, h->scalars, st);
   h->tm.end(st);
-  int rc = scatter_scaling(h, h->w, h->eta, h->wbar);
+  int rc = scatter_scaling(h, h->w, h->eta, h->wbar, /*have_consts=*/L.nsoc > 0);
   if (rc) return rc;
   rc = do_factor(h);
   if (rc) return rc;
-  // predictor: d_comp = -lam o lam
-  h->tm.begin(T_CONE, st);
-  qsk_rhs_cone(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, -1.0, h->r_cone, h->d, h->rhs + n + p, st);
-  h->tm.end(st);
   rc = solve_refined(h, h->rhs);
   if (rc) return rc;
   h->tm.begin(T_CONE, st);
+  // predictor: ds_a, W dz_a, both steps, alpha_aff, mu_aff, sigma
   qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, h->wdz, h->ds, h->scalars, 0,
-                 h->st.step_fraction, h->gr, st);
-  qsk_mu_aff((int)m, h->s, h->z, h->ds, h->sol + n + p, h->deg, h->scalars, h->gr, st);
-  // corrector: d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a)
-  qsk_dcomp(L, h->w, h->eta, h->wbar, h->ds, h->wdz, h->lam_sq, h->dcomp, h->scalars, st);
-  qsk_rhs_cone(L, h->w, h->eta, h->wbar, h->lam, h->dcomp, 1.0, h->r_cone, h->d, h->rhs + n + p, st);
+                 h->st.step_fraction, h->deg, h->gr, st);
+  // corrector: d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a), d = lam \ d_comp, rhs_z = -r_cone - W d
+  qsk_corrector_rhs(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->ds, h->wdz, h->r_cone, nullptr, h->d,
+                    h->rhs + n + p, h->scalars, st);
   h->tm.end(st);
   rc = solve_refined(h, h->rhs);
   if (rc) return rc;
   h->tm.begin(T_CONE, st);
   qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, nullptr, h->ds, h->scalars, 1,
-                 h->st.step_fraction, h->gr, st);
+                 h->st.step_fraction, h->deg, h->gr, st);
   qsk_update_iterate((int)n, (int)p, (int)m, h->x, h->y, h->z, h->s, h->x2, h->y2, h->z2, h->s2, h->sol, h->ds, h->deg,
                      h->scalars, h->gr, st);
   h->tm.end(st);
-  h->launches += 8;
+  h->launches += 5;
   rc = check_launch(h, "ipm_step");
   if (rc) return rc;
   rc = fetch_scalars(h);
@@ -1486,14 +1496,18 @@ static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, dou
   cudaEventCreate(&b);
   auto run = [&]() {
     switch (kernel_id) {
-      case 0: qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->scalars, st); break;
-      case 1: qsk_neg_wtw(h->wp, 2, h->w, h->eta, h->wbar, h->d_pos, h->d_Kx, st); break;
-      case 2: qsk_neg_wtw(h->wp, 1, h->w, h->eta, h->wbar, h->d_pos, h->d_Kx, st); break;
-      case 3: qsk_rhs_cone(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, -1.0, h->r_cone, h->d, h->rhs + n + p, st); break;
+      case 0: qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->wp.c4, h->wp.e2, h->r_cone, h->d,
+                             h->rhs + n + p, h->scalars, st); break;
+      case 1: qsk_neg_wtw(h->wp, 2, h->w, h->eta, h->wbar, h->d_pos, h->d_Kx, st, L.nsoc > 0); break;
+      case 2: qsk_neg_wtw(h->wp, 1, h->w, h->eta, h->wbar, h->d_pos, h->d_Kx, st, L.nsoc > 0); break;
+      case 3: qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, nullptr, nullptr, nullptr, nullptr,
+                             nullptr, h->scalars, st); break;  // scaling + lam o lam alone
       case 4: qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, h->wdz, h->ds, h->scalars, 0,
-                             h->st.step_fraction, h->gr, st); break;
-      case 5: qsk_mu_aff((int)m, h->s, h->z, h->ds, h->sol + n + p, h->deg, h->scalars, h->gr, st); break;
-      case 6: qsk_dcomp(L, h->w, h->eta, h->wbar, h->ds, h->wdz, h->lam_sq, h->dcomp, h->scalars, st); break;
+                             h->st.step_fraction, h->deg, h->gr, st); break;
+      case 5: qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, nullptr, h->tmp_m, h->scalars, 1,
+                             h->st.step_fraction, h->deg, h->gr, st); break;
+      case 6: qsk_corrector_rhs(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->ds, h->wdz, h->r_cone, nullptr, h->tmp_m,
+                                h->w2vz, h->scalars, st); break;
       case 7: {
         ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->x, h->y, h->z, h->s,
                        h->c,   h->b,   h->hv,  h->rhs, h->r_cone, h->scalars, h->gr};
@@ -1513,10 +1527,12 @@ static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, dou
         qsk_kkt_residual(A, st);
         break;
       }
+      case 15: qsk_update_iterate((int)n, (int)p, (int)m, h->x, h->y, h->z, h->s, h->x2, h->y2, h->z2, h->s2, h->sol, h->ds,
+                                  h->deg, h->scalars, h->gr, st); break;
       default: break;
     }
   };
-  if (kernel_id < 0 || kernel_id > 14) return fail(h, QS_E_INVALID, "unknown kernel id");
+  if (kernel_id < 0 || kernel_id > 15) return fail(h, QS_E_INVALID, "unknown kernel id");
   run();  // warm-up
   float ms = 0.f;
   if (!cold) {

@@ -70,8 +70,9 @@ struct ConeLayout {
   const int* soc_ptr;    // [nsoc+1]
   int group;             // lanes cooperating on one small cone (1,2,4,...,32)
   int single;            // -1: each op picks its own decomposition; 0 / 1 force chunked / register-resident
+  int waves;             // persistent grid = waves x the CTAs resident at once (0 = 1; tuning knob QS_CONE_WAVES)
   int nsmall;            // cones handled by lane groups
-  const int* small_ids;  // [nsmall] or nullptr when every cone is small
+  const int* small_ids;  // [nsmall] small cones sorted by dimension, largest first (nullptr: natural order)
   int nbig;              // cones handled by a whole CTA (dim > big threshold)
   const int* big_ids;    // [nbig]
 };

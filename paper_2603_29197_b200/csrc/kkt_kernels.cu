@@ -378,8 +378,8 @@ int orth_blocks(int l) {
 }  // namespace
 
 void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta, const double* wbar,
-                 const i64* positions, double* out, cudaStream_t st) {
-  if (P.nsoc > 0)
+                 const i64* positions, double* out, cudaStream_t st, bool have_consts) {
+  if (P.nsoc > 0 && !have_consts)  // the NT-scaling kernel of the solver leaves c4 / e2 behind
     k_wtw_prepass<<<(P.nsoc * 32 + QS_THREADS - 1) / QS_THREADS, QS_THREADS, 0, st>>>(P.nsoc, P.soc_ptr, wbar, eta,
                                                                                         P.c4, P.e2);
   const int nb_orth = orth_blocks(P.l);

@@ -34,8 +34,9 @@ struct WtwPlan {
 };
 
 // mode: 0 dense slots, 1 explicit int64 positions map, 2 closed-form positions
+// have_consts: P.c4 / P.e2 already hold the constants of this scaling (written by qsk_nt_scaling)
 void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta, const double* wbar,
-                 const i64* positions, double* out, cudaStream_t st);
+                 const i64* positions, double* out, cudaStream_t st, bool have_consts = false);
 void qsk_check_direct_map(const WtwPlan& P, const i64* positions, int* flag, cudaStream_t st);
 
 // KKT assembly on the device: row indices (int32), initial values and the slot -> position map of every column,

@@ -36,14 +36,15 @@ def main(nsoc=10000, qlo=20, qhi=250, l=0, reps=20):
     peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")) else 6650.0
     N = n + m
-    kernels = [  # id, name, algorithmic bytes
-        (0, "nt_scaling(+lam_sq)", 32 * m + 8 * (l + nsoc) + 8 * m),
+    kernels = [  # id, name, algorithmic bytes of the logical ops the kernel covers
+        (0, "nt_scaling+lam_sq+pred_rhs", 40 * m + 8 * (l + nsoc) + 64 * m),
+        (3, "nt_scaling+lam_sq (alone)", 40 * m + 8 * (l + nsoc)),
         (1, "neg_wtw_scatter(direct)", 8 * S + 8 * (m + nsoc)),
         (2, "neg_wtw_scatter(map)", 8 * S + 8 * (m + nsoc)),
-        (3, "rhs_cone(div+W+rhs)", 24 * m + 24 * m + 16 * m),
-        (4, "post_solve(2xW+2xmax_step)", 24 * m + 24 * m + 32 * m),
-        (5, "mu_aff(2 dots)", 32 * m),
-        (6, "dcomp(Winv+prod+rhs)", 24 * m + 24 * m + 32 * m),
+        (4, "post_solve(pred)+mu_aff", 80 * m + 32 * m),
+        (5, "post_solve(corr)", 80 * m),
+        (6, "dcomp+corr_rhs", 80 * m + 64 * m),
+        (15, "update_iterate", 24 * n + 48 * m),
         (7, "residuals(5 spmv+norms)", 12 * (2 * n + 2 * m) + 8 * (3 * n + 4 * m)),
         (8, "apply_w", 24 * m),
         (9, "jordan_product", 24 * m),
