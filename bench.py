@@ -9,16 +9,30 @@ every iteration until the reference's termination test passes).  Workload at
 N=1: C4, the ~1.2e8-KKT-nonzero group-lasso SOCP (10^4 second-order cones of
 size 20..250) -- the configuration BASELINE.json's target is quoted on.
 
-  value  seconds per solve with the problem, KKT system and factor analysis
-         already resident in HBM when the timed region starts (CUDA events);
-  e2e    seconds per Solver(algebra="cuda").setup(...).solve() call starting
-         from HOST NumPy buffers: KKT assembly, ordering, H2D, solve, D2H;
-  roofline   the dominant hot-path kernel (the -W'W generate-and-scatter):
-         algorithmic bytes / CUDA-event time vs the measured HBM peak;
-  cpu_baseline  the CPU oracle (C port of the reference) on a bounded sample.
+  value     seconds per solve with the problem, KKT system and factor analysis
+            already resident in HBM when the timed region starts (CUDA events);
+  e2e       seconds per Solver(algebra="cuda").setup(...).solve() call starting
+            from HOST NumPy buffers: KKT assembly, ordering, H2D, solve, D2H;
+  roofline  the dominant hot-path kernel (the -W'W generate-and-scatter):
+            algorithmic bytes / CUDA-event time vs the measured HBM peak;
+  ladder    the SAME seeded inputs at 1/100, 1/32 and 1/10 of the workload solved by
+            both arms: GPU (public API, host buffers) and the CPU oracle, measured
+            seconds, iterations and objective per rung -- nothing is extrapolated;
+            rungs the CPU cannot finish inside the bench's time budget carry the
+            CPU numbers of the committed offline run (tests/golden/, labelled);
+  cpu_baseline  the CPU oracle (C port of the reference, pinned bitwise to it) on
+            the largest rung that fits ~20 s, measured on this box, threads stated;
+  batch     the north_star's multi-GPU deliverable: 512 independent MPC SOCPs (C5),
+            instance i -> rank i mod N, no data-path collective; instances/s.
 
-N > 1 (torchrun): every rank solves its own independent instance (seed = rank):
-no data-path collective, weak scaling, value = max over ranks.
+N > 1 (torchrun): every rank solves its own independent instance of the workload
+(seed = rank): no data-path collective, weak scaling, value = max over ranks.
+
+--impl reference: the reference's CPU path on the host cores.  The full workload
+takes the CPU hours (the ordering alone grows like size^2.5), so every step is one
+COMPLETE solve of the 1/100 rung (BASELINE.md section 4's first ladder rung); `value`
+is that measured time -- a LOWER BOUND on the CPU time of the full workload
+("lower_bound": true), never scaled.
 """
 
 from __future__ import annotations
@@ -37,15 +51,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name -> (config key, kwargs, CPU sample kwargs, scale = full work / sample work)
-    "C4_group_lasso": ("C4_group_lasso", dict(groups=10_000, qlo=20, qhi=250, samples=2_000, nnz_per_col=3),
-                       dict(groups=16, qlo=20, qhi=250, samples=2_000, nnz_per_col=3)),
-    "C2_lasso": ("C2_lasso", dict(features=100_000, samples=5_000), dict(features=2_000, samples=100)),
-    "C3_portfolio": ("C3_portfolio", dict(assets=100_000, factors=100, sector=100),
-                     dict(assets=2_000, factors=100, sector=100)),
-    "C1_random_qp": ("C1_random_qp", dict(n=2000, p=500, m=4000), dict(n=1000, p=250, m=2000)),
-    "C5_mpc": ("C5_mpc", dict(horizon=50, nx=12, nu=4), dict(horizon=50, nx=12, nu=4)),
+    # name -> (config key, kwargs of the full workload)
+    "C4_group_lasso": ("C4_group_lasso", dict(groups=10_000, qlo=20, qhi=250, samples=2_000, nnz_per_col=3)),
+    "C2_lasso": ("C2_lasso", dict(features=100_000, samples=5_000)),
+    "C3_portfolio": ("C3_portfolio", dict(assets=100_000, factors=100, sector=100)),
+    "C1_random_qp": ("C1_random_qp", dict(n=2000, p=500, m=4000)),
+    "C5_mpc": ("C5_mpc", dict(horizon=50, nx=12, nu=4)),
 }
+
+# Scale ladder: every dimension of the workload scaled together, same generator, same seed,
+# same cone-size distribution.  (label, fraction of the full size, kwargs)
+LADDERS = {
+    "C4_group_lasso": [("1/100", dict(groups=100, qlo=20, qhi=250, samples=20, nnz_per_col=3)),
+                       ("1/32", dict(groups=316, qlo=20, qhi=250, samples=63, nnz_per_col=3)),
+                       ("1/10", dict(groups=1000, qlo=20, qhi=250, samples=200, nnz_per_col=3))],
+    "C2_lasso": [("1/100", dict(features=1_000, samples=50)), ("1/10", dict(features=10_000, samples=500))],
+    "C3_portfolio": [("1/100", dict(assets=1_000, factors=100, sector=100)),
+                     ("1/10", dict(assets=10_000, factors=100, sector=100))],
+    "C1_random_qp": [("1/4", dict(n=500, p=125, m=1000)), ("1/2", dict(n=1000, p=250, m=2000))],
+    "C5_mpc": [("1/1", dict(horizon=50, nx=12, nu=4))],
+}
+BATCH_COUNT = 512  # BASELINE.json configs[4]
 
 
 def peaks():
@@ -53,6 +79,15 @@ def peaks():
     if os.path.exists(path):
         return float(json.load(open(path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_info():
+    info = {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "cpu": ""}
+    try:
+        info["cpu"] = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")][0]
+    except (OSError, IndexError):
+        pass
+    return info
 
 
 class ClockSampler:
@@ -91,79 +126,165 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None, "samples": len(rows), "reasons": reasons}
 
 
+def mapped_repo_libraries():
+    """Shared objects of this repository mapped into the process (the reference arm must show oracle/ only)."""
+    try:
+        libs = {ln.split()[-1] for ln in open("/proc/self/maps") if ".so" in ln and ROOT in ln}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in libs)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+def workload_config(workload, data):
+    """The `config` object of the JSON line; both arms print the same one."""
+    from paper_2603_29197_b200 import configs
+
+    key, full_kw = WORKLOADS[workload]
+    return {"workload": workload, **full_kw, "n": data.n, "p": data.p, "m": data.m, "kkt_nnz": configs.kkt_nnz(data),
+            "l2": "inputs larger than L2 (KKT values and the factor are rewritten every iteration)"}
+
+
 # ------------------------------------------------------------------ CPU arms
-def cpu_solve_sample(workload, threads_note=True):
-    """One oracle solve of the bounded CPU sample; returns (seconds_setup, seconds_solve, iterations, scale, text)."""
+def oracle_solve(data):
+    """One complete CPU solve (reference algorithm: reference AMD, up-looking LDL', refinement, IPM) -> record."""
     from oracle import qsocp_oracle as orc
     from paper_2603_29197_b200 import configs
 
-    key, full_kw, sample_kw = WORKLOADS[workload]
-    d = configs.make(key, **sample_kw)
-    res = orc.solve(d)
-    full_nnz = _full_kkt_nnz(workload)
-    scale = full_nnz / configs.kkt_nnz(d)
-    text = (f"{key} {sample_kw}: KKT nnz {configs.kkt_nnz(d)} of {full_nnz} (1/{scale:.0f}), full solve, "
-            f"{res.iterations} iterations, status {res.status}; seconds scaled linearly in KKT nnz to the full "
-            f"workload (the CPU factorisation grows at least linearly, so this under-states the CPU time)")
-    return res.setup_seconds, res.solve_seconds, res.iterations, scale, text
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):  # "cores: 1" is what runs: no BLAS/OpenMP helper threads
+        t = time.perf_counter()
+        res = orc.solve(data)
+        wall = time.perf_counter() - t
+    it = max(res.iterations, 1)
+    return {"kkt_nnz": configs.kkt_nnz(data), "status": str(res.status), "iterations": int(res.iterations),
+            "objective": float(res.objective), "setup_seconds": float(res.setup_seconds),
+            "solve_seconds": float(res.solve_seconds), "wall_seconds": wall,
+            "cone_kkt_update_us_per_iter": float(res.timers.get("hot_path", 0.0)) / it * 1e6,
+            "factor_seconds": float(res.timers.get("factor", 0.0)), "L_nnz": int(res.timers.get("L_nnz", 0))}
 
 
-_NNZ_CACHE = {}
-
-
-def _full_kkt_nnz(workload):
-    if workload not in _NNZ_CACHE:
-        key, full_kw, _ = WORKLOADS[workload]
-        if key == "C4_group_lasso":  # closed form, avoids generating the full problem in the CPU arm
-            rng = np.random.default_rng(0)
-            q = rng.integers(full_kw["qlo"], full_kw["qhi"] + 1, full_kw["groups"])
-            nf = int((q - 1).sum())
-            ns = full_kw["samples"]
-            n = nf + ns + full_kw["groups"]
-            _NNZ_CACHE[workload] = int(n + nf * full_kw["nnz_per_col"] + ns + ns + (nf + full_kw["groups"])
-                                       + (q * (q + 1) // 2).sum())
-        else:
-            from paper_2603_29197_b200 import configs
-
-            _NNZ_CACHE[workload] = configs.kkt_nnz(configs.make(key, **full_kw))
-    return _NNZ_CACHE[workload]
+def offline_record(workload, label):
+    """CPU numbers of a rung the bench cannot afford to run live: committed by tools/oracle_fullsize.py (measured
+    in the build container, one thread; the file says where)."""
+    name = f"full_{workload}.npz" if label == "full" else f"ladder_{workload}_{label.replace('/', 'of')}.npz"
+    path = os.path.join(ROOT, "tests", "golden", name)
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    timers = json.loads(str(g["timers"]))
+    it = max(int(g["iterations"]), 1)
+    return {"status": str(g["status"]), "iterations": int(g["iterations"]), "objective": float(g["objective"]),
+            "setup_seconds": float(g["setup_seconds"]), "solve_seconds": float(g["solve_seconds"]),
+            "cone_kkt_update_us_per_iter": float(timers.get("hot_path", 0.0)) / it * 1e6,
+            "L_nnz": int(timers.get("L_nnz", 0)), "ordering": str(g["ordering"]) if "ordering" in g.files else
+            "reference AMD (oracle restatement)", "source": f"offline: tests/golden/{name}", "host": json.loads(str(g["host"]))}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (the pinned C/NumPy port of it --
-    the numba reference itself does not exist on the GPU box) on the host cores."""
+    """--impl reference: the reference's CPU path (the pinned C/NumPy port of it -- the numba reference itself does
+    not exist on the GPU box) on the host cores; see the module docstring for what a step is."""
     rank, _, world = dist_env()
     if rank != 0:
         return
     from oracle import qsocp_oracle as orc
+    from paper_2603_29197_b200 import configs
 
     orc.build()
-    times, e2e = [], []
-    text = ""
+    t_begin = time.perf_counter()
+    key, full_kw = WORKLOADS[args.workload]
+    ladder = LADDERS[args.workload]
+    label, kw = ladder[0]
+    sample = configs.make(key, **kw)
+    recs = []
     for k in range(args.warmup + args.steps):
-        st, so, iters, scale, text = cpu_solve_sample(args.workload)
+        r = oracle_solve(sample)
         if k >= args.warmup:
-            times.append(so * scale)
-            e2e.append((st + so) * scale)
-    val = float(np.mean(times))
-    key, full_kw, _ = WORKLOADS[args.workload]
+            recs.append(r)
+    val = float(np.mean([r["solve_seconds"] for r in recs]))
+    e2e = float(np.mean([r["setup_seconds"] + r["solve_seconds"] for r in recs]))
+    rungs = [dict(recs[-1], scale=label, config=kw, cpu_source="measured in this run")]
+    for label2, kw2 in ladder[1:]:  # further rungs, once each, while the budget lasts (each costs ~8x the previous)
+        spent = time.perf_counter() - t_begin
+        if spent + 8.0 * rungs[-1]["wall_seconds"] > args.ref_budget:
+            break
+        rungs.append(dict(oracle_solve(configs.make(key, **kw2)), scale=label2, config=kw2,
+                          cpu_source="measured in this run"))
+    full = offline_record(args.workload, "full")
     line = {
         "impl": "reference", "metric": "ipm_solve_seconds", "value": val, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, **full_kw},
-        "cpu_baseline": {"value": val, "unit": "s", "cores": 1, "kind": "port", "sample": text},
-        "e2e": {"value": float(np.mean(e2e)), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
+        "config": workload_config(args.workload, configs.make(key, **full_kw)),
+        "lower_bound": True,
+        "cpu_baseline": {"value": val, "unit": "s", "cores": 1, "kind": "port", "host": host_info(),
+                         "sample": f"every step = one complete CPU solve of the {label} rung of {args.workload} {kw} "
+                                   f"(KKT nnz {recs[-1]['kkt_nnz']}, {recs[-1]['iterations']} iterations, "
+                                   f"{recs[-1]['status']}); measured, not scaled: a lower bound on the CPU time of the "
+                                   f"full workload"},
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ladder": rungs, "full_workload_cpu": full, "gpu_launches": 0,
+        "native_libraries_mapped": mapped_repo_libraries(),
     }
     print(json.dumps(line))
 
 
 # ------------------------------------------------------------------- GPU arm
+def gpu_ladder(workload, device, cpu_budget, with_cpu):
+    """The same seeded inputs through both arms, rung by rung (measured; see module docstring)."""
+    import paper_2603_29197_b200 as qs
+    from paper_2603_29197_b200 import configs
+    from paper_2603_29197_b200.problem import Settings
+
+    key, full_kw = WORKLOADS[workload]
+    out = []
+    spent = 0.0
+    last = 0.0
+    for label, kw in LADDERS[workload]:
+        d = configs.make(key, **kw)
+        qs.solve(d, Settings(device=device))  # warm-up of this shape (pool growth, graph capture)
+        t = time.perf_counter()
+        r = qs.solve(d, Settings(device=device))
+        wall = time.perf_counter() - t
+        rung = {"scale": label, "config": kw, "kkt_nnz": configs.kkt_nnz(d),
+                "gpu": {"status": r.status.value, "iterations": int(r.iterations), "objective": float(r.objective),
+                        "setup_seconds": float(r.setup_seconds), "solve_seconds": float(r.solve_seconds),
+                        "e2e_seconds": wall}}
+        cpu = None
+        if with_cpu and spent + max(8.0 * last, 1.0) <= cpu_budget:
+            cpu = dict(oracle_solve(d), source="measured in this run (1 thread)")
+            spent += cpu["wall_seconds"]
+            last = cpu["wall_seconds"]
+        else:
+            cpu = offline_record(workload, label)
+        if cpu:
+            rung["cpu"] = cpu
+            rung["iterations_equal"] = cpu["iterations"] == rung["gpu"]["iterations"]
+            rung["objective_rel_diff"] = abs(cpu["objective"] - r.objective) / max(1.0, abs(cpu["objective"]))
+            rung["ratio_solve"] = cpu["solve_seconds"] / r.solve_seconds
+            rung["ratio_e2e"] = (cpu["setup_seconds"] + cpu["solve_seconds"]) / wall
+        out.append(rung)
+    return out
+
+
+def batch_throughput(rank, world, device, count=BATCH_COUNT, workers=8):
+    """C5: `count` independent MPC SOCPs, instance i -> rank i mod world, no data-path collective.  Returns this
+    rank's (seconds, records, mode); the caller takes the max over ranks."""
+    from paper_2603_29197_b200 import configs
+    from paper_2603_29197_b200.batch import shard, solve_shard
+
+    mine = shard(count, rank, world)
+    probs = {i: configs.make("C5_mpc", seed=i) for i in mine}
+    solve_shard([probs[mine[0]]] * min(len(mine), workers), device, workers)  # warm-up
+    t = time.perf_counter()
+    recs, mode = solve_shard([probs[i] for i in mine], device, workers)
+    return time.perf_counter() - t, recs, mode
+
+
 def run_ours(args):
     import torch
 
@@ -178,10 +299,11 @@ def run_ours(args):
     from paper_2603_29197_b200.ipm import DeviceSolver
     from paper_2603_29197_b200.problem import Settings, SolveStatus
 
-    key, full_kw, _ = WORKLOADS[args.workload]
+    key, full_kw = WORKLOADS[args.workload]
     data = configs.make(key, seed=rank, **full_kw)
     settings = Settings(device=local_rank)
     hbm_peak, peak_src = peaks()
+    torch.cuda.set_device(local_rank)
 
     def barrier():
         torch.cuda.synchronize()
@@ -189,10 +311,12 @@ def run_ours(args):
             dist.barrier()
             torch.cuda.synchronize()
 
-    # ---- resident arm: setup once, time K solves with CUDA events on the device
+    # ---- resident arm: setup once, time K solves with CUDA events on the stream the library launches on (a
+    # non-default stream: graph capture is not possible on the legacy NULL stream)
+    stream = torch.cuda.Stream(device=local_rank)
     t0 = time.perf_counter()
     dev = DeviceSolver(data, settings)
-    dev.set_stream(torch.cuda.current_stream().cuda_stream)  # so torch.cuda.Event brackets the library's launches
+    dev.set_stream(stream.cuda_stream)
     setup_seconds = time.perf_counter() - t0
     for _ in range(args.warmup):
         status, iters, _ = dev.run()
@@ -202,14 +326,14 @@ def run_ours(args):
     sampler = ClockSampler(local_rank) if rank == 0 else None
     barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    # the handle launches on its own stream; bracket with full-device synchronisation
     t_start = time.perf_counter()
-    ev[0].record()
+    ev[0].record(stream)
     iters_total = 0
     for _ in range(args.steps):
         status, iters, it = dev.run()
+        assert status is SolveStatus.SOLVED, status
         iters_total += iters
-    ev[1].record()
+    ev[1].record(stream)
     barrier()
     wall = time.perf_counter() - t_start
     dev_seconds = ev[0].elapsed_time(ev[1]) * 1e-3
@@ -240,7 +364,7 @@ def run_ours(args):
     dom = kt["neg_wtw_scatter"]
     iters_per = iters_total / args.steps
     # the dominant kernel inside the timed region: the kkt_update phase (CUDA events in the library around the
-    # prepass + scatter launches) runs once per factorisation = iterations + 1 times per solve
+    # scatter launch) runs once per factorisation = iterations + 1 times per solve
     dom_launches = iters_per + 1
     dom_us_region = phase.get("kkt_update", 0.0) / max(dom_launches, 1) * 1e6
     if dom_us_region > 0:
@@ -249,6 +373,7 @@ def run_ours(args):
     cone_kkt_us = (phase.get("cone", 0.0) + phase.get("kkt_update", 0.0)) / max(iters_per, 1) * 1e6
     alg_iter = 8 * S + 576 * m + 32 * (n + p + m) + 24 * (n + p)  # un-fused algorithmic bytes per iteration
     fstats = dev.factor_stats()
+    graph = dev.graph_stats() if hasattr(dev, "graph_stats") else None
     dev.close()
 
     # ---- end-to-end arm: the public API on host buffers (setup + solve + result read-back), every step
@@ -259,6 +384,7 @@ def run_ours(args):
         return res
 
     e2e_s = float("nan")
+    e2e_setup = e2e_solve = float("nan")
     if args.e2e_steps > 0:  # 0 = skip (profiling runs only; a bench line without e2e is not a result)
         e2e_once()  # warm-up
         barrier()
@@ -267,6 +393,7 @@ def run_ours(args):
             res = e2e_once()
         barrier()
         e2e_s = (time.perf_counter() - te) / args.e2e_steps
+        e2e_setup, e2e_solve = res.setup_seconds, res.solve_seconds
     # bytes per e2e step, counted by the library from the buffers it copies: host -> device = row views of P/A/G
     # (int32 index + fp64 value), c/b/h, the KKT column pointers and the analysis structures (the KKT entries are
     # written by the device); device -> host = the scalar block of every phase and x, y, z, s at the end
@@ -274,7 +401,22 @@ def run_ours(args):
         h2d, d2h = res.timers["h2d_bytes"], res.timers["d2h_bytes"]
     else:
         h2d = d2h = 0
-    knnz = configs.kkt_nnz(data)
+
+    # ---- the batch of independent small instances (C5), sharded over the ranks
+    batch = None
+    if not args.no_batch:
+        barrier()
+        bsec, brecs, bmode = batch_throughput(rank, world, local_rank, args.batch_count)
+        bad = sum(r.status != "Solved" for r in brecs)
+        if world > 1:
+            t = torch.tensor([bsec, float(bad)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
+            bsec, bad = t.tolist()
+        batch = {"workload": "C5_mpc (horizon 50, nx 12, nu 4: n 800, p 600, m 1450, KKT nnz 14806)",
+                 "instances": args.batch_count, "n_gpus": world, "sharding": "instance i -> rank i mod n_gpus, no collective",
+                 "scaling": "strong", "seconds": bsec, "instances_per_s": args.batch_count / bsec, "mode": bmode,
+                 "not_solved": int(bad), "mean_iterations": float(np.mean([r.iterations for r in brecs]))}
 
     if world > 1:
         t = torch.tensor([per_solve, e2e_s], dtype=torch.float64, device="cuda")
@@ -284,40 +426,53 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        from oracle import qsocp_oracle as orc
+    ladder = cpu = None
+    if world == 1 and not args.no_ladder:
+        if not args.no_cpu:
+            from oracle import qsocp_oracle as orc
 
-        orc.build()
-        st, so, ci, scale, text = cpu_solve_sample(args.workload)
-        cpu = {"value": so * scale, "unit": "s", "cores": 1, "kind": "port", "sample": text,
-               "sample_seconds": so, "sample_setup_seconds": st, "scale": scale,
-               "e2e_value": (st + so) * scale}
+            orc.build()
+        ladder = gpu_ladder(args.workload, local_rank, args.cpu_budget, not args.no_cpu)
+        live = [r for r in ladder if r.get("cpu", {}).get("source", "").startswith("measured")]
+        if live:
+            r = live[-1]
+            c = r["cpu"]
+            cpu = {"value": c["solve_seconds"], "unit": "s", "cores": 1, "kind": "port", "host": host_info(),
+                   "sample": f"{r['scale']} rung of {args.workload} {r['config']}: KKT nnz {r['kkt_nnz']}, complete solve, "
+                             f"{c['iterations']} iterations, {c['status']}; measured on this box, not scaled",
+                   "setup_seconds": c["setup_seconds"], "cone_kkt_update_us_per_iter": c["cone_kkt_update_us_per_iter"],
+                   "gpu_same_input": r["gpu"], "ratio_solve_same_input": r["ratio_solve"],
+                   "ratio_e2e_same_input": r["ratio_e2e"], "full_workload_cpu": offline_record(args.workload, "full")}
     line = {
         "metric": "ipm_solve_seconds", "value": per_solve, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_solve * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, **full_kw, "n": n, "p": p, "m": m, "kkt_nnz": configs.kkt_nnz(data),
-                   "l2": "inputs larger than L2 (KKT values 0.97 GB, factor 5.7 GB are rewritten every iteration)"},
+        "config": workload_config(args.workload, data),
         "iterations_per_solve": iters_per, "host_wall_seconds_per_solve": wall / args.steps,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "setup_seconds_resident_arm": setup_seconds},
+                "setup_seconds": e2e_setup, "solve_seconds": e2e_solve, "setup_seconds_resident_arm": setup_seconds},
         "gpu_launches": int(l1 - l0),
         "roofline": {"bound": "hbm", "kernel": "k_neg_wtw<DIRECT> (-W'W generate + scatter into K.values)",
                      "achieved": dom["gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": dom["frac"],
                      "peak_source": peak_src, "traffic": args.traffic, "alg_bytes_per_launch": dom["alg_bytes"],
                      "us_per_launch": dom["us"], "us_per_launch_isolated": dom.get("us_isolated", dom["us"]),
-                     "timing": "CUDA events around the KKT-update phase of every factorisation inside the timed solves "
-                               "(prepass + scatter); 'isolated' = 20 back-to-back launches after the timed region"},
+                     "timing": "CUDA events around the KKT-update phase of every factorisation inside the timed solves; "
+                               "'isolated' = 20 back-to-back launches after the timed region"},
         "hot_path": {"cone_plus_kkt_update_us_per_iter": cone_kkt_us, "alg_bytes_per_iter": alg_iter,
                      "frac_of_hbm_peak_unfused_alg": alg_iter / max(cone_kkt_us, 1e-9) / 1e3 / hbm_peak,
+                     "residual_us_per_iter": phase.get("residual", 0.0) / max(iters_per + 1, 1) * 1e6,
                      "kernels": kt},
         "phase_seconds_per_solve": phase,
         "factor": {k: fstats[k] for k in ("supernodes", "levels", "L_nnz", "factor_flops", "max_front_rows")},
+        "graphs": graph,
         "clocks": clocks,
     }
+    if ladder:
+        line["ladder"] = ladder
     if cpu:
         line["cpu_baseline"] = cpu
+    if batch:
+        line["batch"] = batch
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -331,7 +486,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C4_group_lasso", choices=sorted(WORKLOADS))
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU legs (cpu_baseline, CPU side of the ladder)")
+    ap.add_argument("--no-ladder", action="store_true", help="skip the scale ladder")
+    ap.add_argument("--no-batch", action="store_true", help="skip the C5 batch")
+    ap.add_argument("--batch-count", type=int, default=BATCH_COUNT)
+    ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of CPU oracle work in the ours arm")
+    ap.add_argument("--ref-budget", type=float, default=240.0, help="seconds of CPU work in the reference arm")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     args = ap.parse_args()

@@ -105,6 +105,27 @@ int qs_symbolic_stats(int64_t N, const int64_t* Kp, const int64_t* Ki, int64_t o
  * big_threshold: SOCs larger than this use the block-per-cone path (<=0: default). */
 int qs_set_cones(qs_handle* h, int64_t l, int64_t nsoc, const int64_t* q_host, int64_t big_threshold);
 
+/* The fused per-iteration kernels of qs_step on caller-owned DEVICE vectors (vector-level parity against the
+ * reference's ipm_step intermediates, pkg/src/qsocp/ipm.py:180-234).  Need qs_set_cones.
+ * qs_predictor_rhs: compute_nt_scaling + lam o lam (cones.py:159-184, ipm.py:191), d = lam \ (-lam o lam) and the
+ *   third RHS block rhs_z = -r_cone - W d (ipm.py:180-184).
+ * qs_corrector_rhs: d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a) (ipm.py:209-211), d, rhs_z as above.
+ * qs_post_solve: wdz = W dz, ds = W (d - W dz) (ipm.py:187-188), max_step_to_boundary for (s, ds), (z, dz) with
+ *   check_interior (cones.py:247-299); corrector = 0 also alpha_aff, mu_aff, mu, sigma (ipm.py:195-206), corrector = 1
+ *   alpha (ipm.py:214-218).  out8 = {step_s, step_z, alpha_aff, alpha, mu, mu_aff, sigma, flags}.
+ * qs_update_iterate: the new iterate, finite check, new mu (ipm.py:219-234); sol = (dx, dy, dz).  out2 = {mu, flags}. */
+int qs_predictor_rhs(qs_handle* h, const double* s, const double* z, const double* r_cone, double* w, double* eta,
+                     double* wbar, double* lam, double* lam_sq, double* d, double* rhs_z, int* not_interior_host);
+int qs_corrector_rhs(qs_handle* h, const double* w, const double* eta, const double* wbar, const double* lam,
+                     const double* lam_sq, const double* ds_a, const double* wdz_a, const double* r_cone, double sigma,
+                     double mu, double* dcomp, double* d, double* rhs_z);
+int qs_post_solve(qs_handle* h, const double* w, const double* eta, const double* wbar, const double* d,
+                  const double* dz, const double* s, const double* z, int corrector, double step_fraction, double* wdz,
+                  double* ds, double* out8_host);
+int qs_update_iterate(qs_handle* h, int64_t n, int64_t p, const double* x, const double* y, const double* z,
+                      const double* s, const double* sol, const double* ds, double alpha, double* xo, double* yo,
+                      double* zo, double* so, double* out2_host);
+
 /* ---- per-kernel entry points (dev pointers; unit parity tests, ncu) ------ */
 /* compute_nt_scaling cones.py:159-184; lam_sq may be NULL.  flag_host != NULL forces a sync. */
 int qs_nt_scaling(qs_handle* h, const double* s, const double* z, double* w, double* eta, double* wbar, double* lam,

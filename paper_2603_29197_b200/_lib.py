@@ -67,6 +67,10 @@ SIGNATURES = {
     "qs_bring_to_interior": (C.c_int, [vp, vp, C.c_double, vp, f64p]),
     "qs_compute_mu": (C.c_int, [vp, vp, vp, f64p]),
     "qs_neg_wtw": (C.c_int, [vp, C.c_int] + [vp] * 7),
+    "qs_predictor_rhs": (C.c_int, [vp] * 11 + [C.POINTER(C.c_int)]),
+    "qs_corrector_rhs": (C.c_int, [vp] * 9 + [C.c_double, C.c_double] + [vp] * 3),
+    "qs_post_solve": (C.c_int, [vp] * 8 + [C.c_int, C.c_double, vp, vp, f64p]),
+    "qs_update_iterate": (C.c_int, [vp, C.c_int64, C.c_int64] + [vp] * 6 + [C.c_double] + [vp] * 4 + [f64p]),
     "qs_spmv_csr": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, vp, vp, C.c_int]),
     "qs_spmv_sym_upper": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp]),
     "qs_setup": (C.c_int, [vp] + [C.c_int64] * 5 + [vp] * 13 + [C.POINTER(QsSettings), vp]),

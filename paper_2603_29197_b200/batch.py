@@ -38,6 +38,19 @@ def _default_solve(data, settings):
     return solve(data, settings)
 
 
+def rank_device(rank: int = 0, device_count: int | None = None) -> int:
+    """The GPU of this rank: LOCAL_RANK under torchrun (one process per GPU), else rank mod the visible devices."""
+    import os
+
+    if "LOCAL_RANK" in os.environ:
+        return int(os.environ["LOCAL_RANK"])
+    if device_count is None:
+        from . import _lib
+
+        device_count = max(_lib.load().qs_device_count(), 1)
+    return rank % device_count
+
+
 def pattern_reuse_solver():
     """solve_fn for batches whose instances share one sparsity pattern (MPC trajectories, parametric sweeps): every
     worker thread keeps ONE device handle; the first instance pays setup + analysis, the following ones only upload
@@ -49,6 +62,7 @@ def pattern_reuse_solver():
     from .api import Solver
 
     tls = threading.local()
+    opened = []  # every worker's solver, so close() can release the device handles when the pool is done
 
     def same_pattern(a, b):
         return (a.n, a.m, a.p) == (b.n, b.m, b.p) and a.cone == b.cone and all(
@@ -64,14 +78,25 @@ def pattern_reuse_solver():
             s = Solver("cuda").setup(d.n, d.m, d.p, d.P, d.c, d.A, d.b, d.G, d.h, d.cone.orthant_dim,
                                      len(d.cone.soc_dims), d.cone.soc_dims, **kw)
             tls.solver, tls.settings = s, settings
+            opened.append(s)
         return s.solve()
 
+    def close():
+        for s in opened:
+            s.close()
+        opened.clear()
+
+    solve_fn.close = close
     return solve_fn
 
 
 def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: int = 1, solve_fn=None, group=None,
-                workers: int = 1):
+                workers: int = 1, device: int | None = None):
     """Solve instances {i : i mod world == rank}; gather records on rank 0.
+
+    The rank's GPU is `device` (default: rank_device(rank) = LOCAL_RANK under torchrun); it is written into the
+    Settings every solve of this rank receives, so rank r never lands on device 0 by default.  A failing instance
+    becomes a record with status "Error: ..." -- the gather always completes.
 
     make_instance(i) -> ProblemData.  solve_fn(data, settings) -> SolveResult
     (defaults to the CUDA path on settings.device).  workers > 1 keeps that many instances in flight on this rank's
@@ -81,10 +106,20 @@ def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: 
     (pkg/src/qsocp/bench/runner.py:107-117).  Returns
     (records sorted by index on rank 0 / this rank's records elsewhere, wall seconds of this rank).
     """
+    import dataclasses
+
+    from .problem import Settings
+
     solve_fn = solve_fn or _default_solve
+    if device is None:
+        device = rank_device(rank)
+    settings = dataclasses.replace(settings or Settings(), device=device)
 
     def one(i):
-        res = solve_fn(make_instance(i), settings)
+        try:
+            res = solve_fn(make_instance(i), settings)
+        except Exception as exc:  # noqa: BLE001 -- one bad instance must not hang the other ranks in the gather
+            return InstanceRecord(i, rank, f"Error: {type(exc).__name__}: {exc}", 0, float("nan"), 0.0, 0.0)
         return InstanceRecord(i, rank, getattr(res.status, "value", str(res.status)), int(res.iterations),
                               float(res.objective), float(res.setup_seconds), float(res.solve_seconds))
 
@@ -98,6 +133,8 @@ def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: 
     else:
         mine = [one(i) for i in todo]
     wall = time.perf_counter() - t0
+    if hasattr(solve_fn, "close"):
+        solve_fn.close()
     if world == 1:
         return mine, wall
     import torch.distributed as dist
@@ -110,3 +147,14 @@ def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: 
             raise RuntimeError("batch gather lost or duplicated instances")
         return out, wall
     return mine, wall
+
+
+def solve_shard(problems, device: int, workers: int = 8):
+    """This rank's share of a batch on GPU `device` -> (records, mode description).  Same-pattern instances keep one
+    handle per worker (analysis, index maps and launch graphs are reused; only the numbers are uploaded)."""
+    from .problem import Settings
+
+    fn = pattern_reuse_solver()
+    recs, _ = solve_batch(lambda i: problems[i], len(problems), Settings(device=device), solve_fn=fn, workers=workers,
+                          device=device)
+    return recs, f"{workers} instances in flight, one handle + stream each, pattern reuse (qs_update_values)"

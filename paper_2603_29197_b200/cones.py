@@ -178,6 +178,58 @@ class DeviceCones:
         self._check(self.lib.qs_compute_mu(self.h, self.p(a), self.p(b), C.byref(mu)))
         return mu.value
 
+    # -- the fused kernels of one IPM step (ipm.py:180-234), vector in / vector out
+    def predictor_rhs(self, s, z, r_cone):
+        """-> (NTScalingSet, lam_sq, d = lam \\ (-lam o lam), rhs_z = -r_cone - W d)."""
+        cone = self.cone
+        l, nsoc, m = cone.orthant_dim, cone.soc_count, cone.total_dim
+        a, b, r = self.dev(s), self.dev(z), self.dev(r_cone)
+        w, eta, lam, lsq, d, rz = (self.empty(k) for k in (l, nsoc, m, m, m, m))
+        wbar = self._torch.zeros(max(m, 1), dtype=self._torch.float64, device=self.device)
+        flag = C.c_int(0)
+        self._torch.cuda.synchronize(self.device)
+        self._check(self.lib.qs_predictor_rhs(self.h, self.p(a), self.p(b), self.p(r), self.p(w), self.p(eta),
+                                              self.p(wbar), self.p(lam), self.p(lsq), self.p(d), self.p(rz),
+                                              C.byref(flag)))
+        if flag.value:
+            raise NotInterior("point is not strictly inside the cone")
+        sc = NTScalingSet(cone, self.host(w, l), self.host(eta, nsoc), self.host(wbar, m), self.host(lam, m))
+        return sc, self.host(lsq, m), self.host(d, m), self.host(rz, m)
+
+    def corrector_rhs(self, sc, lam_sq, ds_a, wdz_a, r_cone, sigma, mu):
+        """-> (d_comp, d = lam \\ d_comp, rhs_z = -r_cone - W d)."""
+        m = self.cone.total_dim
+        w, eta, wbar = self._scaling_dev(sc)
+        lam, lsq, a, b, r = (self.dev(v) for v in (sc.lam, lam_sq, ds_a, wdz_a, r_cone))
+        dc, d, rz = self.empty(m), self.empty(m), self.empty(m)
+        self._check(self.lib.qs_corrector_rhs(self.h, self.p(w), self.p(eta), self.p(wbar), self.p(lam), self.p(lsq),
+                                              self.p(a), self.p(b), self.p(r), float(sigma), float(mu), self.p(dc),
+                                              self.p(d), self.p(rz)))
+        return self.host(dc, m), self.host(d, m), self.host(rz, m)
+
+    def post_solve(self, sc, d, dz, s, z, corrector=False, step_fraction=0.99):
+        """-> (wdz = W dz, ds = W (d - W dz), dict of step_s, step_z, alpha_aff, alpha, mu, mu_aff, sigma, flags)."""
+        m = self.cone.total_dim
+        w, eta, wbar = self._scaling_dev(sc)
+        dd, ddz, a, b = (self.dev(v) for v in (d, dz, s, z))
+        wdz, ds = self.empty(m), self.empty(m)
+        out = np.zeros(8)
+        self._check(self.lib.qs_post_solve(self.h, self.p(w), self.p(eta), self.p(wbar), self.p(dd), self.p(ddz),
+                                           self.p(a), self.p(b), int(corrector), float(step_fraction), self.p(wdz),
+                                           self.p(ds), out.ctypes.data_as(C.POINTER(C.c_double))))
+        keys = ("step_s", "step_z", "alpha_aff", "alpha", "mu", "mu_aff", "sigma", "flags")
+        return self.host(wdz, m), self.host(ds, m), dict(zip(keys, out.tolist()))
+
+    def update_iterate(self, x, y, z, s, sol, ds, alpha):
+        """-> (x', y', z', s', mu', flags) with sol = (dx, dy, dz)."""
+        n, p, m = len(x), len(y), self.cone.total_dim
+        a = [self.dev(v) for v in (x, y, z, s, sol, ds)]
+        o = [self.empty(k) for k in (n, p, m, m)]
+        out = np.zeros(2)
+        self._check(self.lib.qs_update_iterate(self.h, n, p, *[self.p(v) for v in a], float(alpha),
+                                               *[self.p(v) for v in o], out.ctypes.data_as(C.POINTER(C.c_double))))
+        return (*[self.host(t, k) for t, k in zip(o, (n, p, m, m))], out[0], int(out[1]))
+
     def neg_wtw_values(self, sc, out=None):
         """Slot values of -W'W in the reference's slot order (cones.py:319-336)."""
         off, _ = slot_layout(self.cone)

@@ -838,6 +838,87 @@ int qs_neg_wtw(qs_handle* h, int mode, const double* w, const double* eta, const
   return check_launch(h, "neg_wtw");
 }
 
+// ---- the fused per-iteration kernels on caller-owned device vectors (vector-level parity tests, ncu)
+// predictor_rhs: compute_nt_scaling + lam o lam + d = lam \ (-lam o lam) + rhs_z = -r_cone - W d
+// (cones.py:159-184, ipm.py:180-184,191-192) -- the first cone kernel of qs_step.
+int qs_predictor_rhs(qs_handle* h, const double* s, const double* z, const double* r_cone, double* w, double* eta,
+                     double* wbar, double* lam, double* lam_sq, double* d, double* rhs_z, int* not_interior_host) {
+  NEED_CONES(h)
+  cudaMemsetAsync(h->scalars + SC_FLAG_NOT_INTERIOR, 0, sizeof(double), h->stream);
+  qsk_nt_scaling(h->L, s, z, w, eta, wbar, lam, lam_sq, h->wp.c4, h->wp.e2, r_cone, d, rhs_z, h->scalars, h->stream);
+  h->launches++;
+  int rc = check_launch(h, "predictor_rhs");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  if (not_interior_host) *not_interior_host = h->scalars_host[SC_FLAG_NOT_INTERIOR] != 0.0;
+  return QS_OK;
+}
+
+// corrector_rhs: d_comp = sigma mu e - lam o lam - (W^-1 ds_a) o (W dz_a), d = lam \ d_comp,
+// rhs_z = -r_cone - W d (ipm.py:180-184,209-212).  dcomp may be null.
+int qs_corrector_rhs(qs_handle* h, const double* w, const double* eta, const double* wbar, const double* lam,
+                     const double* lam_sq, const double* ds_a, const double* wdz_a, const double* r_cone, double sigma,
+                     double mu, double* dcomp, double* d, double* rhs_z) {
+  NEED_CONES(h)
+  h->scalars_host[SC_SIGMA] = sigma;
+  h->scalars_host[SC_MU] = mu;
+  CK(h, cudaMemcpyAsync(h->scalars + SC_SIGMA, h->scalars_host + SC_SIGMA, sizeof(double), cudaMemcpyHostToDevice,
+                        h->stream));
+  CK(h, cudaMemcpyAsync(h->scalars + SC_MU, h->scalars_host + SC_MU, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  qsk_corrector_rhs(h->L, w, eta, wbar, lam, lam_sq, ds_a, wdz_a, r_cone, dcomp, d, rhs_z, h->scalars, h->stream);
+  h->launches++;
+  CK(h, cudaStreamSynchronize(h->stream));  // the pinned mirror is reused by the next fetch
+  return check_launch(h, "corrector_rhs");
+}
+
+// post_solve: wdz = W dz, ds = W (d - W dz), max_step_to_boundary of (s, ds) and (z, dz) with the interior
+// pre-check; predictor (corrector = 0): alpha_aff, mu_aff, mu = s'z/deg, sigma; corrector: alpha
+// (ipm.py:187-188,195-206,214-218).  out8 = {step_s, step_z, alpha_aff, alpha, mu, mu_aff, sigma, flags}.
+int qs_post_solve(qs_handle* h, const double* w, const double* eta, const double* wbar, const double* d,
+                  const double* dz, const double* s, const double* z, int corrector, double step_fraction, double* wdz,
+                  double* ds, double* out8_host) {
+  NEED_CONES(h)
+  clear_flags(h);
+  qsk_post_solve(h->L, w, eta, wbar, d, dz, s, z, wdz, ds, h->scalars, corrector, step_fraction, h->deg, h->gr,
+                 h->stream);
+  h->launches++;
+  int rc = check_launch(h, "post_solve");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  if (out8_host) {
+    const double* sc = h->scalars_host;
+    const double o[8] = {sc[SC_STEP_S], sc[SC_STEP_Z], sc[SC_ALPHA_AFF], sc[SC_ALPHA],
+                         sc[SC_MU],     sc[SC_MU_AFF], sc[SC_SIGMA],     (double)flags_of(sc)};
+    for (int k = 0; k < 8; ++k) out8_host[k] = o[k];
+  }
+  return QS_OK;
+}
+
+// update_iterate: (x, y, z, s) + alpha (dx, dy, dz, ds) with sol = (dx, dy, dz), the finite check and the new
+// mu = s'z/deg (ipm.py:219-234).  out2 = {mu, flags}.
+int qs_update_iterate(qs_handle* h, int64_t n, int64_t p, const double* x, const double* y, const double* z,
+                      const double* s, const double* sol, const double* ds, double alpha, double* xo, double* yo,
+                      double* zo, double* so, double* out2_host) {
+  NEED_CONES(h)
+  clear_flags(h);
+  h->scalars_host[SC_ALPHA] = alpha;
+  CK(h, cudaMemcpyAsync(h->scalars + SC_ALPHA, h->scalars_host + SC_ALPHA, sizeof(double), cudaMemcpyHostToDevice,
+                        h->stream));
+  qsk_update_iterate((int)n, (int)p, h->L.m, x, y, z, s, xo, yo, zo, so, sol, ds, h->deg, h->scalars, h->gr, h->stream);
+  h->launches++;
+  int rc = check_launch(h, "update_iterate");
+  if (rc) return rc;
+  rc = fetch_scalars(h);
+  if (rc) return rc;
+  if (out2_host) {
+    out2_host[0] = h->scalars_host[SC_MU];
+    out2_host[1] = (double)flags_of(h->scalars_host);
+  }
+  return QS_OK;
+}
+
 int qs_spmv_csr(qs_handle* h, int64_t rows, int64_t cols, const int32_t* ptr, const int32_t* idx, const double* val,
                 const double* x, double* y, int accumulate) {
   if (!h) return QS_E_INVALID;

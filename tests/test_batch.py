@@ -26,7 +26,7 @@ def test_shard_is_a_partition():
 
 def _worker(rank, world, port, out):
     sys.path.insert(0, ROOT)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))  # as torchrun sets it
     import torch.distributed as dist
 
     from oracle import qsocp_oracle as orc
@@ -34,8 +34,15 @@ def _worker(rank, world, port, out):
     from paper_2603_29197_b200.batch import solve_batch
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    devices = []
+
+    def solve_fn(d, settings):
+        devices.append(settings.device)  # what the CUDA path would hand to qs_create
+        return orc.solve(d)
+
     recs, wall = solve_batch(lambda i: configs.make("C5_mpc", small=True, seed=i), 6, None, rank, world,
-                             solve_fn=lambda d, s: orc.solve(d))
+                             solve_fn=solve_fn)
+    assert devices == [rank] * 3, devices  # every solve of rank r is placed on GPU r (settings=None included)
     if rank == 0:
         out.put([(r.index, r.rank, r.status, r.iterations, r.objective) for r in recs])
     dist.destroy_process_group()
@@ -85,3 +92,25 @@ def test_worker_pool_keeps_the_order_and_overlaps_instances():
     assert [r.index for r in recs] == list(range(10))
     assert [r.iterations for r in recs] == list(range(10))
     assert peak[0] > 1
+
+
+def test_rank_device_and_error_records(monkeypatch):
+    from types import SimpleNamespace
+
+    from paper_2603_29197_b200.batch import rank_device, solve_batch
+
+    monkeypatch.delenv("LOCAL_RANK", raising=False)
+    assert [rank_device(r, 4) for r in range(6)] == [0, 1, 2, 3, 0, 1]
+    monkeypatch.setenv("LOCAL_RANK", "3")
+    assert rank_device(0, 8) == 3
+    seen = []
+
+    def solve_fn(d, settings):
+        seen.append(settings.device)
+        if d == 2:
+            raise RuntimeError("boom")
+        return SimpleNamespace(status="Solved", iterations=1, objective=0.0, setup_seconds=0.0, solve_seconds=0.0)
+
+    recs, _ = solve_batch(lambda i: i, 4, None, solve_fn=solve_fn, device=5)
+    assert seen == [5, 5, 5, 5]
+    assert [r.status for r in recs] == ["Solved", "Solved", "Error: RuntimeError: boom", "Solved"]

@@ -74,3 +74,83 @@ def test_full_size_c4_is_bitwise_reproducible():
     assert a.iterations == b.iterations and a.objective == b.objective
     for k in "xyzs":
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+# ---- iteration-count / objective / residual parity with the reference's algorithm at BASELINE size -----------------
+# tests/golden/full_<workload>.npz and ladder_<workload>_<rung>.npz: the CPU oracle (pinned bitwise to the reference)
+# run offline on the same seeded instance by tools/oracle_fullsize.py (minutes to hours of one CPU core).
+def _golden_runs():
+    import glob
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return sorted(os.path.basename(p) for p in glob.glob(os.path.join(here, "full_*.npz"))
+                  + glob.glob(os.path.join(here, "ladder_*.npz")))
+
+
+def _solve_with_mu_trace(d):
+    from paper_2603_29197_b200.ipm import DeviceSolver, _objective
+
+    dev = DeviceSolver(d)
+    try:
+        mus = []
+        # the hook receives the iterate after initialisation and after every step, as the reference's does
+        status, iters, it = dev.run(iterate_hook=lambda it: mus.append(it.mu))
+        return status, iters, it, _objective(d, it.x), np.array(mus)
+    finally:
+        dev.close()
+
+
+@pytest.mark.parametrize("fname", _golden_runs())
+def test_full_size_matches_the_offline_reference_run(fname):
+    """north_star contract at BASELINE size: iteration count within +-1 of the reference's algorithm, final objective
+    and residual norms to a relative 1e-6, the barrier-parameter trace iterate by iterate."""
+    import json
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", fname))
+    name, kw = str(g["workload"]), json.loads(str(g["config"]))
+    d = configs.make(name, **kw)
+    status, iters, it, obj, mus = _solve_with_mu_trace(d)
+    assert status is SolveStatus.SOLVED and str(g["status"]) == "Solved"
+    ref_iters = int(g["iterations"])
+    assert abs(iters - ref_iters) <= 1, (iters, ref_iters)
+    ref_obj = float(g["objective"])
+    assert abs(obj - ref_obj) <= 1e-6 * max(1.0, abs(ref_obj)), (obj, ref_obj)
+    # residual norms of the returned point (scipy restatement), against the reference's, relative to the scales of
+    # its termination test (ipm.py:106-119): both are ~1e-9 of those scales, so they agree to 1e-6 of them
+    P, A, G = _csc(d.P), _csc(d.A), _csc(d.G)
+    Pf = P + sp.triu(P, 1).T
+    inf = lambda v: float(np.max(np.abs(v), initial=0.0))
+    nPx, nAty, nGtz, nc, nAx, nb, nGx, nh = (float(v) for v in g["norms"])
+    r_dual = Pf @ it.x + d.c + A.T @ it.y + G.T @ it.z
+    r_eq = A @ it.x - d.b
+    r_cone = G @ it.x + it.s - d.h
+    assert abs(inf(r_dual) - float(g["norm_r_dual"])) <= 1e-6 * max(nPx, nAty, nGtz, nc, 1e-300)
+    assert abs(inf(r_eq) - float(g["norm_r_eq"])) <= 1e-6 * max(nAx, nb, 1.0)
+    assert abs(inf(r_cone) - float(g["norm_r_cone"])) <= 1e-6 * max(nGx, nh, inf(it.s), 1.0)
+    assert abs(float(it.s @ it.z) - float(g["gap"])) <= 1e-6 * max(abs(ref_obj), 1.0)
+    for key, v in (("x_norm", it.x), ("s_norm", it.s), ("z_norm", it.z)):
+        assert abs(np.linalg.norm(v) - float(g[key])) <= 1e-5 * max(1.0, float(g[key])), key
+    k = min(mus.size, g["trace_mu"].size)
+    assert k >= ref_iters  # the traces overlap over (at least) every iteration but the last
+    np.testing.assert_allclose(mus[:k], g["trace_mu"][:k], rtol=1e-4, atol=1e-14)
+
+
+@pytest.mark.parametrize("rung", [0, 1])
+def test_ladder_rungs_match_the_oracle_live(oracle, rung):
+    """The bench's scale ladder (1/100 and 1/32 of C4, same generator and seed): the CPU oracle and the GPU on the same
+    input, here and now -- iterations equal +-1, objective 1e-6, iterate 1e-5."""
+    import bench
+
+    label, kw = bench.LADDERS["C4_group_lasso"][rung]
+    d = configs.make("C4_group_lasso", **kw)
+    ref = oracle.solve(d)
+    res = qs.solve(d)
+    assert res.status is SolveStatus.SOLVED and ref.status == "Solved"
+    assert abs(res.iterations - ref.iterations) <= 1, (label, res.iterations, ref.iterations)
+    assert abs(res.objective - ref.objective) <= 1e-6 * max(1.0, abs(ref.objective))
+    if res.iterations == ref.iterations:
+        for k in "xs":
+            a, b = getattr(res, k), getattr(ref, k)
+            assert np.max(np.abs(a - b)) <= 1e-5 * max(1.0, np.max(np.abs(b))), k

@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 
 
 def main():
-    from bench import WORKLOADS
+    from bench import LADDERS, WORKLOADS
     from oracle import qsocp_oracle as orc
     from paper_2603_29197_b200 import configs
 
@@ -31,8 +31,16 @@ def main():
     ap.add_argument("--perm-cache", default=None)
     ap.add_argument("--time-limit", type=float, default=48 * 3600.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--rung", default=None, help="a rung of bench.LADDERS[workload] (e.g. 1/10) instead of the full size; "
+                                                 "written to tests/golden/ladder_<workload>_<rung>.npz")
+    ap.add_argument("--product-perm", action="store_true",
+                    help="take the fill-reducing permutation from the product's host ordering (cone-block AMD) instead "
+                         "of the reference's AMD, whose cost grows like size^2.5 on dense SOC blocks (117 s at 1/10 "
+                         "of C4); the numerics (KKT, LDL', refinement, IPM) stay the oracle's.  Recorded in the file.")
     args = ap.parse_args()
     key, full_kw = WORKLOADS[args.workload][:2]
+    if args.rung:
+        full_kw = dict(LADDERS[args.workload])[args.rung]
     t0 = time.time()
     d = configs.make(key, **full_kw)
     print(f"generated {args.workload} {full_kw}: n={d.n} p={d.p} m={d.m} in {time.time()-t0:.1f}s", flush=True)
@@ -43,6 +51,23 @@ def main():
     if args.perm_cache and os.path.exists(args.perm_cache):
         perm = np.load(args.perm_cache)
         print("ordering loaded from", args.perm_cache, flush=True)
+    elif args.product_perm:
+        import paper_2603_29197_b200 as qs  # noqa: F401  (host C++ ordering only; no GPU involved)
+        from paper_2603_29197_b200 import ordering as pord
+        from paper_2603_29197_b200.kkt import assemble_kkt as product_assemble
+
+        t = time.time()
+        kk = product_assemble(d)
+        dims = np.asarray(d.cone.soc_dims, np.int64)
+        starts = np.ascontiguousarray(d.n + d.p + d.cone.orthant_dim + np.concatenate([[0], np.cumsum(dims)[:-1]]),
+                                      dtype=np.int64) if dims.size else None
+        perm, stats = pord.analyze(kk.matrix.cols, kk.matrix.col_pointers, kk.matrix.row_indices, "amd",
+                                   clique_starts=starts, clique_sizes=dims if dims.size else None)
+        t_amd = time.time() - t
+        print(f"product ordering (cone-block AMD, host C++): {t_amd:.1f}s, predicted L nnz {stats['L_nnz']:.3g}", flush=True)
+        if args.perm_cache:
+            np.save(args.perm_cache, perm)
+        del kk
     else:
         t = time.time()
         K = orc.assemble_kkt(dd).matrix
@@ -69,7 +94,8 @@ def main():
         host["cpu"] = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")][0]
     except (OSError, IndexError):
         pass
-    out = args.out or os.path.join(ROOT, "tests", "golden", f"full_{args.workload}.npz")
+    name = f"ladder_{args.workload}_{args.rung.replace('/', 'of')}.npz" if args.rung else f"full_{args.workload}.npz"
+    out = args.out or os.path.join(ROOT, "tests", "golden", name)
     np.savez_compressed(
         out, workload=np.array(args.workload), config=np.array(json.dumps(full_kw)), status=np.array(res.status),
         iterations=np.array(res.iterations), objective=np.array(res.objective), trace_mu=np.array(mus),
@@ -80,7 +106,9 @@ def main():
         s_norm=np.array(float(np.linalg.norm(res.s))), z_norm=np.array(float(np.linalg.norm(res.z))),
         setup_seconds=np.array(res.setup_seconds + t_amd), solve_seconds=np.array(res.solve_seconds),
         amd_seconds=np.array(t_amd), timers=np.array(json.dumps(res.timers)), host=np.array(json.dumps(host)),
-        factor_count=np.array(res.factor_count), solve_count=np.array(res.solve_count))
+        factor_count=np.array(res.factor_count), solve_count=np.array(res.solve_count),
+        ordering=np.array("product cone-block AMD (permutation handed to the oracle)" if args.product_perm
+                          else "reference AMD (oracle restatement)"))
     print(f"{args.workload}: {res.status} in {res.iterations} iterations, objective {res.objective:.12g}, "
           f"setup {res.setup_seconds + t_amd:.1f}s solve {res.solve_seconds:.1f}s -> {out}", flush=True)
 
