@@ -29,10 +29,11 @@ N > 1 (torchrun): every rank solves its own independent instance of the workload
 (seed = rank): no data-path collective, weak scaling, value = max over ranks.
 
 --impl reference: the reference's CPU path on the host cores.  The full workload
-takes the CPU hours (the ordering alone grows like size^2.5), so every step is one
-COMPLETE solve of the 1/100 rung (BASELINE.md section 4's first ladder rung); `value`
-is that measured time -- a LOWER BOUND on the CPU time of the full workload
-("lower_bound": true), never scaled.
+takes the CPU about an hour (the reference ordering alone grows like size^2.5), so
+every step is one COMPLETE solve of a ladder rung -- the largest one that fits
+(warmup + steps) times into --ref-budget seconds; `value` is that measured time: a
+LOWER BOUND on the CPU time of the full workload ("lower_bound": true), never scaled.
+The same-input ratios are in the ours arm's `ladder`.
 """
 
 from __future__ import annotations
@@ -40,6 +41,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # the C5 batch keeps > 8 streams busy (before CUDA starts)
 import subprocess
 import sys
 import tempfile
@@ -198,22 +201,34 @@ def run_reference(args):
     t_begin = time.perf_counter()
     key, full_kw = WORKLOADS[args.workload]
     ladder = LADDERS[args.workload]
-    label, kw = ladder[0]
+    nsteps = args.warmup + args.steps
+    # the sample = the LARGEST rung whose complete solve, repeated warmup + steps times, fits the budget; found by
+    # climbing the ladder (each rung costs ~10x the one below, measured as we go; every climb is itself a
+    # measured ladder point)
+    pick = 0
+    rungs = [dict(oracle_solve(configs.make(key, **ladder[0][1])), scale=ladder[0][0], config=ladder[0][1],
+                  cpu_source="measured in this run")]
+    while pick + 1 < len(ladder):
+        left = args.ref_budget - (time.perf_counter() - t_begin)
+        if (nsteps + 1) * 10.0 * rungs[pick]["wall_seconds"] > left:
+            break
+        pick += 1
+        rungs.append(dict(oracle_solve(configs.make(key, **ladder[pick][1])), scale=ladder[pick][0],
+                          config=ladder[pick][1], cpu_source="measured in this run"))
+    label, kw = ladder[pick]
     sample = configs.make(key, **kw)
     recs = []
-    for k in range(args.warmup + args.steps):
+    for k in range(nsteps):
         r = oracle_solve(sample)
         if k >= args.warmup:
             recs.append(r)
     val = float(np.mean([r["solve_seconds"] for r in recs]))
     e2e = float(np.mean([r["setup_seconds"] + r["solve_seconds"] for r in recs]))
-    rungs = [dict(recs[-1], scale=label, config=kw, cpu_source="measured in this run")]
-    for label2, kw2 in ladder[1:]:  # further rungs, once each, while the budget lasts (each costs ~8x the previous)
-        spent = time.perf_counter() - t_begin
-        if spent + 8.0 * rungs[-1]["wall_seconds"] > args.ref_budget:
-            break
-        rungs.append(dict(oracle_solve(configs.make(key, **kw2)), scale=label2, config=kw2,
-                          cpu_source="measured in this run"))
+    if pick + 1 < len(ladder):  # one more rung for the ladder, once, if what is left of the budget allows
+        left = args.ref_budget - (time.perf_counter() - t_begin)
+        if 12.0 * rungs[pick]["wall_seconds"] <= left:
+            rungs.append(dict(oracle_solve(configs.make(key, **ladder[pick + 1][1])), scale=ladder[pick + 1][0],
+                              config=ladder[pick + 1][1], cpu_source="measured in this run"))
     full = offline_record(args.workload, "full")
     line = {
         "impl": "reference", "metric": "ipm_solve_seconds", "value": val, "unit": "s", "n_gpus": args.gpus,
@@ -491,7 +506,7 @@ def main():
     ap.add_argument("--no-batch", action="store_true", help="skip the C5 batch")
     ap.add_argument("--batch-count", type=int, default=BATCH_COUNT)
     ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of CPU oracle work in the ours arm")
-    ap.add_argument("--ref-budget", type=float, default=240.0, help="seconds of CPU work in the reference arm")
+    ap.add_argument("--ref-budget", type=float, default=420.0, help="seconds of CPU work in the reference arm")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from the committed ncu capture")
     args = ap.parse_args()

@@ -9,6 +9,11 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+# Batches of small instances keep many streams busy at once; the driver maps streams onto 8 hardware queues by
+# default, which caps the overlap at 8 instances (measured: 125 -> 373 instances/s at C5 with 32 queues).  Only
+# effective when set before the process creates its CUDA context; an explicit setting of the user wins.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 
 from .errors import CudaUnavailable, DimensionMismatch, NotInterior, NumericalError

@@ -64,6 +64,87 @@ enum QsScalar {
   SC_COUNT = 48
 };
 
+// ------------------------------------------------------------ instance batches
+// Batched small-problem mode: B instances with ONE sparsity pattern live in B equal slots of one
+// device arena, QS_BSTRIDE bytes apart; slot b is a byte-for-byte copy of slot 0's layout (pattern arrays included),
+// so the address of anything belonging to instance b is the address in slot 0 plus b * QS_BSTRIDE.  A batched launch
+// is the ordinary launch with gridDim.z = B: every kernel begins with QS_BATCH(...) over its pointer arguments
+// (and structs of pointers), which moves them to the slot of blockIdx.z.  gridDim.z == 1 is the ordinary solver.
+#define QS_BSTRIDE (size_t(1) << 25)  // 32 MiB per instance: "small" means the whole handle fits
+
+// qs_moved(x, off): pointers move by `off` bytes (null stays null; T may be const), structs of pointers move their
+// members (they provide  __device__ void shift(size_t off)), numbers stay.  By value and back by assignment, so
+// __restrict__-qualified kernel parameters are fine.
+template <class T>
+__device__ __forceinline__ T* qs_moved(T* p, size_t off) {
+  return p ? (T*)((char*)p + off) : p;
+}
+template <class T>
+__device__ __forceinline__ typename std::enable_if<std::is_arithmetic<T>::value || std::is_enum<T>::value, T>::type
+qs_moved(T v, size_t) {
+  return v;
+}
+template <class T>
+__device__ __forceinline__ typename std::enable_if<std::is_class<T>::value, T>::type qs_moved(T s, size_t off) {
+  s.shift(off);
+  return s;
+}
+// used inside the shift() members
+template <class T>
+__device__ __forceinline__ void qs_shift(size_t off, T& x) {
+  x = qs_moved(x, off);
+}
+#define QS_FE_1(m, x) m(x)
+#define QS_FE_2(m, x, ...) m(x) QS_FE_1(m, __VA_ARGS__)
+#define QS_FE_3(m, x, ...) m(x) QS_FE_2(m, __VA_ARGS__)
+#define QS_FE_4(m, x, ...) m(x) QS_FE_3(m, __VA_ARGS__)
+#define QS_FE_5(m, x, ...) m(x) QS_FE_4(m, __VA_ARGS__)
+#define QS_FE_6(m, x, ...) m(x) QS_FE_5(m, __VA_ARGS__)
+#define QS_FE_7(m, x, ...) m(x) QS_FE_6(m, __VA_ARGS__)
+#define QS_FE_8(m, x, ...) m(x) QS_FE_7(m, __VA_ARGS__)
+#define QS_FE_9(m, x, ...) m(x) QS_FE_8(m, __VA_ARGS__)
+#define QS_FE_10(m, x, ...) m(x) QS_FE_9(m, __VA_ARGS__)
+#define QS_FE_11(m, x, ...) m(x) QS_FE_10(m, __VA_ARGS__)
+#define QS_FE_12(m, x, ...) m(x) QS_FE_11(m, __VA_ARGS__)
+#define QS_FE_13(m, x, ...) m(x) QS_FE_12(m, __VA_ARGS__)
+#define QS_FE_14(m, x, ...) m(x) QS_FE_13(m, __VA_ARGS__)
+#define QS_FE_15(m, x, ...) m(x) QS_FE_14(m, __VA_ARGS__)
+#define QS_FE_16(m, x, ...) m(x) QS_FE_15(m, __VA_ARGS__)
+#define QS_FE_17(m, x, ...) m(x) QS_FE_16(m, __VA_ARGS__)
+#define QS_FE_18(m, x, ...) m(x) QS_FE_17(m, __VA_ARGS__)
+#define QS_FE_19(m, x, ...) m(x) QS_FE_18(m, __VA_ARGS__)
+#define QS_FE_20(m, x, ...) m(x) QS_FE_19(m, __VA_ARGS__)
+#define QS_FE_21(m, x, ...) m(x) QS_FE_20(m, __VA_ARGS__)
+#define QS_FE_22(m, x, ...) m(x) QS_FE_21(m, __VA_ARGS__)
+#define QS_FE_23(m, x, ...) m(x) QS_FE_22(m, __VA_ARGS__)
+#define QS_FE_24(m, x, ...) m(x) QS_FE_23(m, __VA_ARGS__)
+#define QS_FE_PICK(_1, _2, _3, _4, _5, _6, _7, _8, _9, _10, _11, _12, _13, _14, _15, _16, _17, _18, _19, _20, _21, _22, _23, _24, NAME, ...) NAME
+#define QS_FOR_EACH(m, ...) QS_FE_PICK(__VA_ARGS__, QS_FE_24, QS_FE_23, QS_FE_22, QS_FE_21, QS_FE_20, QS_FE_19, QS_FE_18, QS_FE_17, QS_FE_16, QS_FE_15, QS_FE_14, QS_FE_13, QS_FE_12, QS_FE_11, QS_FE_10, QS_FE_9, QS_FE_8, QS_FE_7, QS_FE_6, QS_FE_5, QS_FE_4, QS_FE_3, QS_FE_2, QS_FE_1)(m, __VA_ARGS__)
+#define QS_MV_(x) x = qs_moved(x, qs_boff_);
+#define QS_BATCH(...)                                               \
+  if (gridDim.z > 1 && blockIdx.z > 0) {                            \
+    const size_t qs_boff_ = (size_t)blockIdx.z * QS_BSTRIDE;        \
+    QS_FOR_EACH(QS_MV_, __VA_ARGS__)                                \
+  }
+
+// Host side: the batch size of the launches issued by this thread (1 outside qs_batch_* calls).
+extern thread_local int qs_tls_batch;
+inline dim3 qs_grid(dim3 g) {
+  g.z = (unsigned)qs_tls_batch;
+  return g;
+}
+// memset / device-to-device copy of the same range in every slot
+inline cudaError_t qs_memset_b(void* p, int value, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  if (qs_tls_batch <= 1) return cudaMemsetAsync(p, value, bytes, st);
+  return cudaMemset2DAsync(p, QS_BSTRIDE, value, bytes, (size_t)qs_tls_batch, st);
+}
+inline cudaError_t qs_copy_b(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  if (qs_tls_batch <= 1) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
+  return cudaMemcpy2DAsync(dst, QS_BSTRIDE, src, QS_BSTRIDE, bytes, (size_t)qs_tls_batch, cudaMemcpyDeviceToDevice, st);
+}
+
 // --------------------------------------------------------------- cone layout
 struct ConeLayout {
   int m, l, nsoc;
@@ -75,6 +156,11 @@ struct ConeLayout {
   const int* small_ids;  // [nsmall] small cones sorted by dimension, largest first (nullptr: natural order)
   int nbig;              // cones handled by a whole CTA (dim > big threshold)
   const int* big_ids;    // [nbig]
+  __device__ void shift(size_t off) {
+    qs_shift(off, soc_ptr);
+    qs_shift(off, small_ids);
+    qs_shift(off, big_ids);
+  }
 };
 
 // ------------------------------------------------------------ group policies
@@ -216,6 +302,10 @@ enum { RED_SUM = 0, RED_MIN = 1, RED_MAX = 2, RED_AMAX = 3 };
 struct GridRed {
   double* partial;    // [>= gridDim.x * K]
   unsigned* counter;  // zero before the launch; left zero afterwards
+  __device__ void shift(size_t off) {
+    qs_shift(off, partial);
+    qs_shift(off, counter);
+  }
 };
 
 // The reduction operators of a launch are COMPILE-TIME constants (RedOps<RED_MIN, RED_MAX, ...>): after

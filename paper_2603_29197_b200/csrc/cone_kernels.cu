@@ -31,6 +31,7 @@ struct NoAcc {};
 // reducing ops is paid once per warp instead of once per cone.
 template <int G, bool RESIDENT, class Op>
 __global__ void __launch_bounds__(QS_THREADS, RESIDENT ? 2 : 3) cone_kernel(ConeLayout L, Op op, int nb_orth, int nb_small, int nb_big) {
+  QS_BATCH(L, op);
   typename Op::Acc acc;
   op.init(acc);
   const int b = blockIdx.x;
@@ -130,7 +131,7 @@ void launch(const ConeLayout& L, const Op& op, cudaStream_t st) {
     if (nbs > 2 * cap) nbs = 2 * cap;
     const int grid = nb_orth + (int)nbs + nb_big;
     if (grid == 0) return;
-    kern<<<grid, QS_THREADS, 0, st>>>(L, op, nb_orth, (int)nbs, nb_big);
+    kern<<<qs_grid(grid), QS_THREADS, 0, st>>>(L, op, nb_orth, (int)nbs, nb_big);
   };
 #define QS_CASE(GG)                                                                 \
   case GG:                                                                          \
@@ -182,6 +183,21 @@ struct NtRhsOp {
   double* d;
   double* rhs_z;
   double* scalars;
+  __device__ void shift(size_t off) {
+    qs_shift(off, s);
+    qs_shift(off, z);
+    qs_shift(off, w);
+    qs_shift(off, eta);
+    qs_shift(off, wbar);
+    qs_shift(off, lam);
+    qs_shift(off, lam_sq);
+    qs_shift(off, c4);
+    qs_shift(off, e2);
+    qs_shift(off, r_cone);
+    qs_shift(off, d);
+    qs_shift(off, rhs_z);
+    qs_shift(off, scalars);
+  }
   struct Acc {
     int bad;
   };
@@ -334,6 +350,13 @@ struct ApplyWOp {
   const double* u;
   double* out;
   int inverse;
+  __device__ void shift(size_t off) {
+    qs_shift(off, w);
+    qs_shift(off, eta);
+    qs_shift(off, wbar);
+    qs_shift(off, u);
+    qs_shift(off, out);
+  }
   typedef NoAcc Acc;
   __device__ void init(Acc&) const {}
   __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
@@ -375,6 +398,11 @@ struct JordanProductOp {
   const double* u;
   const double* v;
   double* out;
+  __device__ void shift(size_t off) {
+    qs_shift(off, u);
+    qs_shift(off, v);
+    qs_shift(off, out);
+  }
   typedef NoAcc Acc;
   __device__ void init(Acc&) const {}
   __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
@@ -406,6 +434,11 @@ struct JordanDivideOp {
   const double* lam;
   const double* v;
   double* out;
+  __device__ void shift(size_t off) {
+    qs_shift(off, lam);
+    qs_shift(off, v);
+    qs_shift(off, out);
+  }
   typedef NoAcc Acc;
   __device__ void init(Acc&) const {}
   __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
@@ -452,6 +485,12 @@ struct MaxStepOp {
   double* scalars;
   int slot_step, slot_viol;
   GridRed gr;
+  __device__ void shift(size_t off) {
+    qs_shift(off, u);
+    qs_shift(off, du);
+    qs_shift(off, scalars);
+    qs_shift(off, gr);
+  }
   struct Acc {
     double step, viol;
   };
@@ -518,6 +557,11 @@ struct ShiftOp {
   const double* scalars;
   int slot;
   double scale;
+  __device__ void shift(size_t off) {
+    qs_shift(off, u);
+    qs_shift(off, out);
+    qs_shift(off, scalars);
+  }
   typedef NoAcc Acc;
   __device__ void init(Acc&) const {}
   __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
@@ -566,6 +610,20 @@ struct CorrRhsOp {
   double* d;
   double* rhs_z;
   const double* scalars;
+  __device__ void shift(size_t off) {
+    qs_shift(off, w);
+    qs_shift(off, eta);
+    qs_shift(off, wbar);
+    qs_shift(off, lam);
+    qs_shift(off, lam_sq);
+    qs_shift(off, ds_a);
+    qs_shift(off, wdz_a);
+    qs_shift(off, r_cone);
+    qs_shift(off, dcomp);
+    qs_shift(off, d);
+    qs_shift(off, rhs_z);
+    qs_shift(off, scalars);
+  }
   typedef NoAcc Acc;
   __device__ void init(Acc&) const {}
   __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
@@ -698,6 +756,19 @@ struct PostSolveOp {
   double step_fraction;
   double deg;
   GridRed gr;
+  __device__ void shift(size_t off) {
+    qs_shift(off, w);
+    qs_shift(off, eta);
+    qs_shift(off, wbar);
+    qs_shift(off, d);
+    qs_shift(off, dz);
+    qs_shift(off, s);
+    qs_shift(off, z);
+    qs_shift(off, wdz);
+    qs_shift(off, ds);
+    qs_shift(off, scalars);
+    qs_shift(off, gr);
+  }
   struct Acc {
     double step_s, step_z, viol_s, viol_z, sz, sdz, dsz, dsdz;
   };
@@ -885,6 +956,13 @@ struct ApplyW2Op {
   const double* wbar;
   const double* u;
   double* out;
+  __device__ void shift(size_t off) {
+    qs_shift(off, w);
+    qs_shift(off, eta);
+    qs_shift(off, wbar);
+    qs_shift(off, u);
+    qs_shift(off, out);
+  }
   typedef NoAcc Acc;
   __device__ void init(Acc&) const {}
   __device__ void orthant(Acc&, const ConeLayout& L, int tid, int nth) const {
@@ -960,6 +1038,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_update_iterate(int n, int p, int
   // it' = it + alpha (dx, dy, dz, ds); mu' = s'.z' / deg; finite check (ipm.py:220-234).  The new iterate goes to
   // (xo, yo, zo, so): the reference builds `nxt` and raises before it replaces `it` (ipm.py:219-229), so a failed
   // step must leave the last good iterate intact -- the host swaps the buffers only when no flag is raised.
+  QS_BATCH(x, y, z, s, xo, yo, zo, so, sol, ds, scalars, gr);
   const double a = scalars[SC_ALPHA];
   const bool bad_step = scalars[SC_FLAG_BAD_STEP] != 0.0;  // alpha <= 0 or non-finite: nothing to apply
   double v[2] = {0.0, 0.0};
@@ -1004,6 +1083,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_update_iterate(int n, int p, int
 
 __global__ void __launch_bounds__(QS_THREADS) k_dot(int m, const double* a, const double* b, double scale, double* out,
                                                     GridRed gr) {
+  QS_BATCH(a, b, out, gr);
   double v[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) v[0] += a[i] * b[i];
   using Ops = RedOps<RED_SUM>;
@@ -1079,9 +1159,9 @@ void qsk_update_iterate(int n, int p, int m, const double* x, const double* y, c
                         double* xo, double* yo, double* zo, double* so, const double* sol, const double* ds, double deg,
                         double* scalars, GridRed gr, cudaStream_t st) {
   i64 big = n > m ? n : m;
-  k_update_iterate<<<vec_grid(big), QS_THREADS, 0, st>>>(n, p, m, x, y, z, s, xo, yo, zo, so, sol, ds, deg, scalars, gr);
+  k_update_iterate<<<qs_grid(vec_grid(big)), QS_THREADS, 0, st>>>(n, p, m, x, y, z, s, xo, yo, zo, so, sol, ds, deg, scalars, gr);
 }
 
 void qsk_dot(int m, const double* a, const double* b, double scale, double* out, GridRed gr, cudaStream_t st) {
-  k_dot<<<vec_grid(m), QS_THREADS, 0, st>>>(m, a, b, scale, out, gr);
+  k_dot<<<qs_grid(vec_grid(m)), QS_THREADS, 0, st>>>(m, a, b, scale, out, gr);
 }

@@ -25,6 +25,7 @@ enum { MODE_SLOTS = 0, MODE_MAP = 1, MODE_DIRECT = 2 };
 // per-cone c = sum wbar^2 (all entries, head included) and eta^2
 __global__ void __launch_bounds__(QS_THREADS) k_wtw_prepass(int nsoc, const int* soc_ptr, const double* wbar,
                                                             const double* eta, double* c4, double* e2) {
+  QS_BATCH(soc_ptr, wbar, eta, c4, e2);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= nsoc) return;
   const int o = soc_ptr[warp], q = soc_ptr[warp + 1] - o;
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(QS_THREADS)
               const i64* __restrict__ slot_start, const i64* __restrict__ positions,
               const i64* __restrict__ kp_conic, const int* __restrict__ g_ptr, const double* __restrict__ g_val,
               double* __restrict__ out) {
+  QS_BATCH(w, wbar, soc_ptr, cone_of_col, tile_ptr, c4, e2, slot_start, positions, kp_conic, g_ptr, g_val, out);
   if ((int)blockIdx.x < nb_orth) {
     // orthant diagonal: slot i holds -(w_i^2)                    (cones.py:324-326)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l; i += nb_orth * blockDim.x) {
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(QS_THREADS)
                      const int* __restrict__ tile_ptr, const double* __restrict__ c4, const double* __restrict__ e2,
                      const i64* __restrict__ slot_start, const i64* __restrict__ kstart,
                      const int* __restrict__ g_ptr, const double* __restrict__ g_val, double* __restrict__ out) {
+  QS_BATCH(w, wbar, soc_ptr, cone_of_col, tile_ptr, c4, e2, slot_start, kstart, g_ptr, g_val, out);
   if ((int)blockIdx.x < nb_orth) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l; i += nb_orth * blockDim.x) {
       const double v = -(w[i] * w[i]);
@@ -288,6 +291,7 @@ __global__ void __launch_bounds__(QS_THREADS)
 __global__ void __launch_bounds__(QS_THREADS)
     k_check_direct(int l, int nb_orth, const int* soc_ptr, const int* cone_of_col, const int* tile_ptr,
                    const i64* slot_start, const i64* positions, const i64* kp_conic, int* flag) {
+  QS_BATCH(soc_ptr, cone_of_col, tile_ptr, slot_start, positions, kp_conic, flag);
   int bad = 0;
   if ((int)blockIdx.x < nb_orth) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < l; i += nb_orth * blockDim.x)
@@ -314,6 +318,7 @@ __global__ void __launch_bounds__(QS_THREADS)
     k_kkt_fill(int n, int p, int m, int l, Csr Pu, Csr Ar, Csr Gr, const int* __restrict__ soc_ptr,
                const int* __restrict__ cone_of_col, const i64* __restrict__ slot_start, const i64* __restrict__ Kp,
                int* __restrict__ Ki, double* __restrict__ Kx, i64* __restrict__ pos) {
+  QS_BATCH(Pu, Ar, Gr, soc_ptr, cone_of_col, slot_start, Kp, Ki, Kx, pos);
   const i64 col = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (col >= (i64)n + p + m) return;
@@ -380,7 +385,7 @@ int orth_blocks(int l) {
 void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta, const double* wbar,
                  const i64* positions, double* out, cudaStream_t st, bool have_consts) {
   if (P.nsoc > 0 && !have_consts)  // the NT-scaling kernel of the solver leaves c4 / e2 behind
-    k_wtw_prepass<<<(P.nsoc * 32 + QS_THREADS - 1) / QS_THREADS, QS_THREADS, 0, st>>>(P.nsoc, P.soc_ptr, wbar, eta,
+    k_wtw_prepass<<<qs_grid((P.nsoc * 32 + QS_THREADS - 1) / QS_THREADS), QS_THREADS, 0, st>>>(P.nsoc, P.soc_ptr, wbar, eta,
                                                                                         P.c4, P.e2);
   const int nb_orth = orth_blocks(P.l);
   const int grid = nb_orth + P.ntiles;
@@ -398,7 +403,7 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
                       (size_t)QS_WTW_SCOLS * (3 * sizeof(double) + 5 * sizeof(int));
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      kern<<<nb_orth + nt, QS_THREADS, sm, st>>>(P.l, nb_orth, w, wbar, P.soc_ptr, P.cone_of_col, tp, P.c4, P.e2,
+      kern<<<qs_grid(nb_orth + nt), QS_THREADS, sm, st>>>(P.l, nb_orth, w, wbar, P.soc_ptr, P.cone_of_col, tp, P.c4, P.e2,
                                                  P.slot_start, P.kstart, P.g_ptr, P.g_val, out);
     };
     if (nb_orth + nt == 0) return;
@@ -418,7 +423,7 @@ void qsk_neg_wtw(const WtwPlan& P, int mode, const double* w, const double* eta,
   const size_t smem = (size_t)mc * (5 * sizeof(double) + 4 * sizeof(int)) + 16 + (size_t)wcap * sizeof(double);
   auto launch = [&](auto kern, const i64* pos, const i64* kpc) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    kern<<<grid, QS_THREADS, smem, st>>>(P.l, nb_orth, mc, wcap, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,
+    kern<<<qs_grid(grid), QS_THREADS, smem, st>>>(P.l, nb_orth, mc, wcap, w, wbar, P.soc_ptr, P.cone_of_col, P.tile_ptr,
                                          P.c4, P.e2, P.slot_start, pos, kpc, P.g_ptr, P.g_val, out);
   };
   if (mode == MODE_SLOTS) {
@@ -437,7 +442,7 @@ void qsk_kkt_fill(const WtwPlan& P, int n, int p, const Csr& Pu, const Csr& Ar, 
                   double* Kx, i64* pos, cudaStream_t st) {
   const i64 N = (i64)n + p + P.m;
   const i64 blocks = (N * 32 + QS_THREADS - 1) / QS_THREADS;
-  k_kkt_fill<<<(unsigned)blocks, QS_THREADS, 0, st>>>(n, p, P.m, P.l, Pu, Ar, Gr, P.soc_ptr, P.cone_of_col,
+  k_kkt_fill<<<qs_grid((unsigned)blocks), QS_THREADS, 0, st>>>(n, p, P.m, P.l, Pu, Ar, Gr, P.soc_ptr, P.cone_of_col,
                                                       P.slot_start, Kp, Ki, Kx, pos);
 }
 
@@ -445,6 +450,6 @@ void qsk_check_direct_map(const WtwPlan& P, const i64* positions, int* flag, cud
   const int nb_orth = orth_blocks(P.l);
   const int grid = nb_orth + P.ntiles;
   if (grid == 0) return;
-  k_check_direct<<<grid, QS_THREADS, 0, st>>>(P.l, nb_orth, P.soc_ptr, P.cone_of_col, P.tile_ptr, P.slot_start,
+  k_check_direct<<<qs_grid(grid), QS_THREADS, 0, st>>>(P.l, nb_orth, P.soc_ptr, P.cone_of_col, P.tile_ptr, P.slot_start,
                                               positions, P.kp_conic, flag);
 }

@@ -36,6 +36,7 @@ __device__ __forceinline__ Front front_of(const DevSym& S, int s, double* L, dou
 
 // K entry -> panel offset (run once at analysis)
 __global__ void __launch_bounds__(LDL_THREADS) k_build_amap(int N, const i64* Kp, const int* Ki, DevSym S, i64* amap) {
+  QS_BATCH(Kp, Ki, S, amap);
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (col >= N) return;
   const int b = S.iperm[col];
@@ -67,11 +68,13 @@ __global__ void __launch_bounds__(LDL_THREADS) k_build_amap(int N, const i64* Kp
 
 __global__ void __launch_bounds__(LDL_THREADS) k_scatter_values(i64 nnz, const double* __restrict__ Kx,
                                                                 const i64* __restrict__ amap, double* __restrict__ L) {
+  QS_BATCH(Kx, amap, L);
   for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < nnz; p += (i64)gridDim.x * blockDim.x)
     L[amap[p]] = Kx[p];
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_add_reg(int N, DevSym S, const double* reg, double* L) {
+  QS_BATCH(S, reg, L);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
     const int s = S.sup_of[j];
     const int lc = j - S.col0[s];
@@ -90,6 +93,7 @@ __global__ void __launch_bounds__(LDL_THREADS) k_add_reg(int N, DevSym S, const 
 // whole warp striding over the child's rows.
 __global__ void __launch_bounds__(LDL_THREADS)
     k_extend_add(DevSym S, const SlabItem* items, double* L, double* U) {
+  QS_BATCH(S, items, L, U);
   const SlabItem it = items[blockIdx.x];
   const int s = it.front;
   const Front f = front_of(S, s, L, U);
@@ -141,6 +145,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 template <int TPR>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_extend_add_list(DevSym S, AsmLists A, const EaItem* items, i64 slot0, i64 nitems, double* L, double* U) {
+  QS_BATCH(S, A, items, L, U);
   const i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / TPR;
   const int lane = threadIdx.x & (TPR - 1);
   if (TPR == 32 ? w >= nitems : false) return;
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 // List-driven forward-solve gather: `tpr` lanes per slot sum the slot's child contributions in a fixed order.
 __global__ void __launch_bounds__(LDL_THREADS)
     k_gather_fwd_list(AsmLists A, i64 slot0, i64 nslots, int tpr, double* xw, double* B) {
+  QS_BATCH(A, xw, B);
   const i64 g = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / tpr;
   const int lane = threadIdx.x & (tpr - 1);
   const unsigned mask = tpr == 32 ? 0xffffffffu : (((1u << tpr) - 1u) << (threadIdx.x & 31 & ~(tpr - 1)));
@@ -231,6 +237,7 @@ template <int G>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_leaf_factor(DevSym S, const int* list, int count, double* L, double* U, double* Dg, const double* reg,
                   double dyn_eps, double* scalars) {
+  QS_BATCH(S, list, L, U, Dg, reg, scalars);
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / G, lane = threadIdx.x & (G - 1);
   if (w >= count) return;
   const unsigned mask = leaf_mask<G>();
@@ -260,6 +267,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 template <int G>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_leaf_fwd(DevSym S, const int* list, int count, const double* L, const double* xw, double* B) {
+  QS_BATCH(S, list, L, xw, B);
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / G, lane = threadIdx.x & (G - 1);
   if (w >= count) return;
   const int s = list[w];
@@ -271,6 +279,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 template <int G>
 __global__ void __launch_bounds__(LDL_THREADS)
     k_leaf_bwd(DevSym S, const int* list, int count, const double* L, double* xw) {
+  QS_BATCH(S, list, L, xw);
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / G, lane = threadIdx.x & (G - 1);
   if (w >= count) return;
   const unsigned mask = leaf_mask<G>();
@@ -285,10 +294,10 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 #define QS_LEAF_DISPATCH(kern, grid, ...)                                                 \
   switch (leaf_group) {                                                                   \
-    case 4: kern<4><<<grid(4), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;                 \
-    case 8: kern<8><<<grid(8), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;                 \
-    case 16: kern<16><<<grid(16), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;              \
-    default: kern<32><<<grid(32), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;              \
+    case 4: kern<4><<<qs_grid(grid(4)), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;                 \
+    case 8: kern<8><<<qs_grid(grid(8)), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;                 \
+    case 16: kern<16><<<qs_grid(grid(16)), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;              \
+    default: kern<32><<<qs_grid(grid(32)), LDL_THREADS, 0, st>>>(__VA_ARGS__); break;              \
   }
 
 // One CTA per front of the level (children already assembled by k_extend_add):
@@ -352,6 +361,7 @@ __device__ void front_factor_body(const DevSym& S, int s, double* L, double* U, 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_front_factor(DevSym S, const int* list, double* L, double* U, double* Dg, const double* reg, double dyn_eps,
                    double* scalars) {
+  QS_BATCH(S, list, L, U, Dg, reg, scalars);
   front_factor_body(S, list[blockIdx.x], L, U, Dg, reg, dyn_eps, scalars);
 }
 
@@ -373,6 +383,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 __global__ void __launch_bounds__(LDL_THREADS)
     k_blk_diag(DevSym S, const int* list, int count, int kb, double* L, double* Dg, const double* reg, double dyn_eps,
                double* scalars) {
+  QS_BATCH(S, list, L, Dg, reg, scalars);
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= count) return;
   const int s = list[w];
@@ -421,6 +432,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_blk_panel(DevSym S, const int* list, int kb, double* L, const double* Dg) {
+  QS_BATCH(S, list, L, Dg);
   const int s = list[blockIdx.y];
   const Front f = front_of(S, s, L, nullptr);
   if (kb >= f.ns) return;
@@ -479,6 +491,7 @@ template <bool SCHUR>
 __global__ void __launch_bounds__(LDL_THREADS, 3)
     k_blk_update(DevSym S, const int* list, const TileItem* tiles, int kb, int left, double* L, double* U,
                  const double* Dg) {
+  QS_BATCH(S, list, tiles, L, U, Dg);
   // SCHUR mode runs over an exact tile list built at analysis (no empty CTAs); PANEL mode keeps the lockstep grid
   TileItem item{0, 0, 0};
   if (SCHUR) item = tiles[blockIdx.x];
@@ -602,6 +615,7 @@ __global__ void __launch_bounds__(LDL_THREADS, 3)
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_zero_cb(DevSym S, const int* list, double* B) {
+  QS_BATCH(S, list, B);
   const int s = list[blockIdx.x];
   if (S.childptr[s + 1] != S.childptr[s]) return;
   const int nu = (int)(S.rowptr[s + 1] - S.rowptr[s]) - (S.col0[s + 1] - S.col0[s]);
@@ -612,6 +626,7 @@ __global__ void __launch_bounds__(LDL_THREADS) k_zero_cb(DevSym S, const int* li
 // ownership scheme as k_extend_add (warp w of a slab owns front row c_lo + w).
 __global__ void __launch_bounds__(LDL_THREADS)
     k_gather_fwd(DevSym S, const SlabItem* items, double* xw, double* B) {
+  QS_BATCH(S, items, xw, B);
   const SlabItem it = items[blockIdx.x];
   const int s = it.front;
   const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
@@ -654,6 +669,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 // ---- blocked triangular solves for the large fronts (lockstep over the level)
 __global__ void __launch_bounds__(32) k_fwd_diag(DevSym S, const int* list, int kb, const double* L, double* xw) {
+  QS_BATCH(S, list, L, xw);
   const int s = list[blockIdx.x];
   const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
   if (kb >= ns) return;
@@ -671,6 +687,7 @@ __global__ void __launch_bounds__(32) k_fwd_diag(DevSym S, const int* list, int 
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_fwd_update(DevSym S, const int* list, int kb, const double* L, double* xw, double* B) {
+  QS_BATCH(S, list, L, xw, B);
   const int s = list[blockIdx.y];
   const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
   if (kb >= ns) return;
@@ -696,6 +713,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 __global__ void __launch_bounds__(LDL_THREADS)
     k_bwd_partial(DevSym S, const int* list, const i64* poff, int kb, const double* L, const double* xw,
                   double* partial) {
+  QS_BATCH(S, list, poff, L, xw, partial);
   const int s = list[blockIdx.y];
   const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
   if (kb >= ns) return;
@@ -727,6 +745,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 __global__ void __launch_bounds__(32)
     k_bwd_diag(DevSym S, const int* list, const i64* poff, int kb, const double* L, double* xw,
                const double* partial) {
+  QS_BATCH(S, list, poff, L, xw, partial);
   const int s = list[blockIdx.x];
   const int c0 = S.col0[s], ns = S.col0[s + 1] - c0;
   if (kb >= ns) return;
@@ -755,6 +774,7 @@ __global__ void __launch_bounds__(32)
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_cluster_fwd(DevSym S, const int* list, const double* L, double* xw, double* B) {
+  QS_BATCH(S, list, L, xw, B);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int QS_CL = (int)cluster.num_blocks();
@@ -814,6 +834,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_cluster_bwd(DevSym S, const int* list, const double* L, double* xw) {
+  QS_BATCH(S, list, L, xw);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int QS_CL = (int)cluster.num_blocks();
@@ -896,10 +917,12 @@ __device__ void solve_fwd_body(const DevSym& S, int s, const double* L, double* 
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_solve_fwd(DevSym S, const int* list, const double* L, double* xw, double* B) {
+  QS_BATCH(S, list, L, xw, B);
   solve_fwd_body(S, list[blockIdx.x], L, xw, B);
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_solve_diag(int N, const double* Dg, double* xw) {
+  QS_BATCH(Dg, xw);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) xw[j] /= Dg[j];
 }
 
@@ -931,6 +954,7 @@ __device__ void solve_bwd_body(const DevSym& S, int s, const double* L, double* 
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_solve_bwd(DevSym S, const int* list, const double* L, double* xw) {
+  QS_BATCH(S, list, L, xw);
   solve_bwd_body(S, list[blockIdx.x], L, xw);
 }
 
@@ -945,11 +969,19 @@ struct ChainArgs {
   const i64* eaptr;         // [nlevels+1] extend-add item ranges
   const EaItem* eaitems;
   const i64* lvslot;        // [nlevels+1] slot ranges
+  __device__ void shift(size_t off) {
+    qs_shift(off, smallptr);
+    qs_shift(off, small_list);
+    qs_shift(off, eaptr);
+    qs_shift(off, eaitems);
+    qs_shift(off, lvslot);
+  }
 };
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_chain_factor(DevSym S, AsmLists A, ChainArgs C, double* L, double* U, double* Dg, const double* reg, double dyn_eps,
                    double* scalars) {
+  QS_BATCH(S, A, C, L, U, Dg, reg, scalars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int lv = C.lv0; lv < C.lv1; ++lv) {
     // extend-add of the level: a warp per (column slot) item, children in list order
@@ -978,6 +1010,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 
 __global__ void __launch_bounds__(LDL_THREADS)
     k_chain_fwd(DevSym S, AsmLists A, ChainArgs C, const double* L, double* xw, double* B) {
+  QS_BATCH(S, A, C, L, xw, B);
   for (int lv = C.lv0; lv < C.lv1; ++lv) {
     for (i64 g = C.lvslot[lv] + threadIdx.x; g < C.lvslot[lv + 1]; g += blockDim.x) {  // thread per slot
       double acc = 0.0;
@@ -995,6 +1028,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_chain_bwd(DevSym S, ChainArgs C, const double* L, double* xw) {
+  QS_BATCH(S, C, L, xw);
   for (int lv = C.lv1 - 1; lv >= C.lv0; --lv)
     for (int k = C.smallptr[lv]; k < C.smallptr[lv + 1]; ++k) {
       solve_bwd_body(S, C.small_list[k], L, xw);
@@ -1003,9 +1037,11 @@ __global__ void __launch_bounds__(LDL_THREADS) k_chain_bwd(DevSym S, ChainArgs C
 }
 
 __global__ void __launch_bounds__(LDL_THREADS) k_permute_in(int N, const int* perm, const double* rhs, double* xw) {
+  QS_BATCH(perm, rhs, xw);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) xw[j] = rhs[perm[j]];
 }
 __global__ void __launch_bounds__(LDL_THREADS) k_permute_out(int N, const int* perm, const double* xw, double* sol) {
+  QS_BATCH(perm, xw, sol);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) sol[perm[j]] = xw[j];
 }
 
@@ -1385,7 +1421,7 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
     return "out of device memory for the LDL' factor (panels " + std::to_string(lsz * 8 >> 20) + " MiB, updates " +
            std::to_string(usz * 8 >> 20) + " MiB)";
   }
-  k_build_amap<<<(unsigned)((N * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>((int)N, d_Kp, d_Ki, D,
+  k_build_amap<<<qs_grid((unsigned)((N * 32 + LDL_THREADS - 1) / LDL_THREADS)), LDL_THREADS, 0, st>>>((int)N, d_Kp, d_Ki, D,
                                                                                               amap);
   cudaStreamSynchronize(st);  // host vectors above must outlive the async copies
   if (cudaGetLastError() != cudaSuccess) return "LDL' analysis kernels failed";
@@ -1442,14 +1478,14 @@ void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
 void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t st) {
   cudaMemsetAsync(L, 0, S.Loff[S.nsup] * 8, st);
   if (S.Uoff[S.nsup] > 0) cudaMemsetAsync(U, 0, S.Uoff[S.nsup] * 8, st);
-  k_scatter_values<<<grid_for(knnz), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
-  k_add_reg<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D, reg, L);
+  k_scatter_values<<<qs_grid(grid_for(knnz)), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
+  k_add_reg<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, D, reg, L);
   auto leaf_grid = [&](int g) { return (unsigned)(((i64)n_leaf * g + LDL_THREADS - 1) / LDL_THREADS); };
   if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_factor, leaf_grid, D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars)
   for (int lv = 0; lv < S.nlevels; ++lv) {
     if (chain_end[lv] > lv + 1) {  // a run of narrow levels: one single-CTA launch
       const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
-      k_chain_factor<<<1, LDL_THREADS, 0, st>>>(D, A, C, L, U, Dg, reg, dyn_eps, scalars);
+      k_chain_factor<<<qs_grid(1), LDL_THREADS, 0, st>>>(D, A, C, L, U, Dg, reg, dyn_eps, scalars);
       lv = chain_end[lv] - 1;
       continue;
     }
@@ -1461,18 +1497,18 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
       const EaItem* itp = direct ? nullptr : d_eaitems + eaptr[lv];
       if (nit > 0) {
         if (ea_wide[lv])
-          k_extend_add_list<32><<<(unsigned)((nit * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+          k_extend_add_list<32><<<qs_grid((unsigned)((nit * 32 + LDL_THREADS - 1) / LDL_THREADS)), LDL_THREADS, 0, st>>>(
               D, A, itp, lvslot[lv], nit, L, U);
         else
-          k_extend_add_list<4><<<(unsigned)((nit * 4 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+          k_extend_add_list<4><<<qs_grid((unsigned)((nit * 4 + LDL_THREADS - 1) / LDL_THREADS)), LDL_THREADS, 0, st>>>(
               D, A, itp, lvslot[lv], nit, L, U);
       }
     } else if (nslab > 0) {
-      k_extend_add<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
+      k_extend_add<<<qs_grid(nslab), LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], L, U);
     }
     const int cnt = smallptr[lv + 1] - smallptr[lv];
     if (cnt > 0)
-      k_front_factor<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, U, Dg, reg, dyn_eps, scalars);
+      k_front_factor<<<qs_grid(cnt), LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, U, Dg, reg, dyn_eps, scalars);
     // blocked fronts of this level, in chunks that fit gridDim.y
     for (int b0 = blkptr[lv]; b0 < blkptr[lv + 1]; b0 += 65535) {
       const int nb_fronts = std::min(65535, blkptr[lv + 1] - b0);
@@ -1485,20 +1521,20 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
         if (left && kb > 0) {  // bring block column kb up to date with the pivots [0, kb)
           const int nti = (mx_nr - kb + TS - 1) / TS;
           dim3 gu(nti, nb_fronts);
-          k_blk_update<false><<<gu, LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 1, L, U, Dg);
+          k_blk_update<false><<<qs_grid(gu), LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 1, L, U, Dg);
         }
-        k_blk_diag<<<(nb_fronts * 32 + LDL_THREADS - 1) / LDL_THREADS, LDL_THREADS, 0, st>>>(D, lst, nb_fronts, kb, L, Dg,
+        k_blk_diag<<<qs_grid((nb_fronts * 32 + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(D, lst, nb_fronts, kb, L, Dg,
                                                                                               reg, dyn_eps, scalars);
         const int rows_below = mx_nr - kb - 1;
         if (rows_below > 0) {
           dim3 gp((rows_below + LDL_THREADS - 1) / LDL_THREADS, nb_fronts);
-          k_blk_panel<<<gp, LDL_THREADS, 0, st>>>(D, lst, kb, L, Dg);
+          k_blk_panel<<<qs_grid(gp), LDL_THREADS, 0, st>>>(D, lst, kb, L, Dg);
         }
         const int cols_left = mx_ns - kb - 1;
         if (!left && cols_left > 0) {
           const int ntj = (cols_left + TS - 1) / TS, nti = (mx_nr - kb - 1 + TS - 1) / TS;
           dim3 gu(ntj * nti, nb_fronts);
-          k_blk_update<false><<<gu, LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 0, L, U, Dg);
+          k_blk_update<false><<<qs_grid(gu), LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 0, L, U, Dg);
         }
       }
     }
@@ -1506,19 +1542,19 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
     const i64 ntile = tileptr[lv + 1] - tileptr[lv];
     for (i64 t0 = 0; t0 < ntile; t0 += (i64)1 << 30) {
       const unsigned cnt2 = (unsigned)std::min<i64>((i64)1 << 30, ntile - t0);
-      k_blk_update<true><<<cnt2, LDL_THREADS, 0, st>>>(D, nullptr, d_tiles + tileptr[lv] + t0, 0, 0, L, U, Dg);
+      k_blk_update<true><<<qs_grid(cnt2), LDL_THREADS, 0, st>>>(D, nullptr, d_tiles + tileptr[lv] + t0, 0, 0, L, U, Dg);
     }
   }
 }
 
 void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st) {
-  k_permute_in<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, d_rhs, xw);
+  k_permute_in<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, D.perm, d_rhs, xw);
   auto leaf_grid = [&](int g) { return (unsigned)(((i64)n_leaf * g + LDL_THREADS - 1) / LDL_THREADS); };
   if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_fwd, leaf_grid, D, d_leaf, n_leaf, L, xw, B)
   for (int lv = 0; lv < S.nlevels; ++lv) {
     if (chain_end[lv] > lv + 1) {
       const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
-      k_chain_fwd<<<1, LDL_THREADS, 0, st>>>(D, A, C, L, xw, B);
+      k_chain_fwd<<<qs_grid(1), LDL_THREADS, 0, st>>>(D, A, C, L, xw, B);
       lv = chain_end[lv] - 1;
       continue;
     }
@@ -1526,13 +1562,13 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
     if (use_lists) {
       const i64 nsl = lvslot[lv + 1] - lvslot[lv];
       if (nsl > 0)
-        k_gather_fwd_list<<<(unsigned)((nsl * lv_tpr[lv] + LDL_THREADS - 1) / LDL_THREADS), LDL_THREADS, 0, st>>>(
+        k_gather_fwd_list<<<qs_grid((unsigned)((nsl * lv_tpr[lv] + LDL_THREADS - 1) / LDL_THREADS)), LDL_THREADS, 0, st>>>(
             A, lvslot[lv], nsl, lv_tpr[lv], xw, B);
     } else if (nslab > 0) {
-      k_gather_fwd<<<nslab, LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], xw, B);
+      k_gather_fwd<<<qs_grid(nslab), LDL_THREADS, 0, st>>>(D, d_slabs + slabptr[lv], xw, B);
     }
     const int cnt = smallptr[lv + 1] - smallptr[lv];
-    if (cnt > 0) k_solve_fwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw, B);
+    if (cnt > 0) k_solve_fwd<<<qs_grid(cnt), LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw, B);
     const int nblk_lv = blkptr[lv + 1] - blkptr[lv];
     // few large fronts (the root): one clustered launch; thousands of fronts: the lockstep path below, which keeps
     // every SM streaming panels (a CTA per front walking its own blocks is latency-bound: 9.2 vs 5.1 ms at C4)
@@ -1544,24 +1580,24 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
       const int nbf = std::min(65535, blkptr[lv + 1] - b0);
       const int* lst = d_blk + b0;
       // childless blocked fronts start their contribution vector from zero (the others were set by the gather)
-      k_zero_cb<<<nbf, LDL_THREADS, 0, st>>>(D, lst, B);
+      k_zero_cb<<<qs_grid(nbf), LDL_THREADS, 0, st>>>(D, lst, B);
       for (int kb = 0; kb < blk_max_ns[lv]; kb += NB) {
-        k_fwd_diag<<<nbf, 32, 0, st>>>(D, lst, kb, L, xw);
+        k_fwd_diag<<<qs_grid(nbf), 32, 0, st>>>(D, lst, kb, L, xw);
         const int rows_below = blk_max_nr[lv] - kb - 1;
         if (rows_below > 0) {
           dim3 g((rows_below + LDL_THREADS - 1) / LDL_THREADS, nbf);
-          k_fwd_update<<<g, LDL_THREADS, 0, st>>>(D, lst, kb, L, xw, B);
+          k_fwd_update<<<qs_grid(g), LDL_THREADS, 0, st>>>(D, lst, kb, L, xw, B);
         }
       }
     }
   }
-  k_solve_diag<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, Dg, xw);
+  k_solve_diag<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, Dg, xw);
   // chain_start[e - 1] = first level of the chain that ends at level e - 1 (or -1)
   for (int lv = S.nlevels - 1; lv >= 0; --lv) {
     if (chain_start_of_end[lv] >= 0) {
       const int b = chain_start_of_end[lv];
       const ChainArgs C{b, lv + 1, d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
-      k_chain_bwd<<<1, LDL_THREADS, 0, st>>>(D, C, L, xw);
+      k_chain_bwd<<<qs_grid(1), LDL_THREADS, 0, st>>>(D, C, L, xw);
       lv = b;
       continue;
     }
@@ -1579,16 +1615,16 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
         const int rows_below = blk_max_nr[lv] - kb - 1;
         if (rows_below > 0) {
           dim3 g((rows_below + LDL_THREADS - 1) / LDL_THREADS, nbf);
-          k_bwd_partial<<<g, LDL_THREADS, 0, st>>>(D, lst, po, kb, L, xw, partial);
+          k_bwd_partial<<<qs_grid(g), LDL_THREADS, 0, st>>>(D, lst, po, kb, L, xw, partial);
         }
-        k_bwd_diag<<<nbf, 32, 0, st>>>(D, lst, po, kb, L, xw, partial);
+        k_bwd_diag<<<qs_grid(nbf), 32, 0, st>>>(D, lst, po, kb, L, xw, partial);
       }
     }
     const int cnt = smallptr[lv + 1] - smallptr[lv];
-    if (cnt > 0) k_solve_bwd<<<cnt, LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw);
+    if (cnt > 0) k_solve_bwd<<<qs_grid(cnt), LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, xw);
   }
   if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_bwd, leaf_grid, D, d_leaf, n_leaf, L, xw)
-  k_permute_out<<<grid_for(N), LDL_THREADS, 0, st>>>((int)N, D.perm, xw, d_sol);
+  k_permute_out<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, D.perm, xw, d_sol);
 }
 
 int LinSys::launches_per_factor() const {

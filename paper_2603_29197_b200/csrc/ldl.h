@@ -34,6 +34,21 @@ struct DevSym {
   const int* sup_of;
   const int* iperm;
   const int* perm;
+  __device__ void shift(size_t off) {
+    qs_shift(off, col0);
+    qs_shift(off, rowptr);
+    qs_shift(off, rowidx);
+    qs_shift(off, childptr);
+    qs_shift(off, child);
+    qs_shift(off, relptr);
+    qs_shift(off, rel);
+    qs_shift(off, Loff);
+    qs_shift(off, Uoff);
+    qs_shift(off, Boff);
+    qs_shift(off, sup_of);
+    qs_shift(off, iperm);
+    qs_shift(off, perm);
+  }
 };
 
 // extend-add work item: front `front`, columns [c_lo, c_lo + 8)
@@ -61,6 +76,16 @@ struct AsmLists {
   const int* slot_row;    // [nslots] local row / column of the slot inside its front
   const i64* bandptr;     // [nsup+1] offsets into bandstart (only children of banded fronts have entries)
   const int* bandstart;
+  __device__ void shift(size_t off) {
+    qs_shift(off, gptr);
+    qs_shift(off, gsrc);
+    qs_shift(off, gchild);
+    qs_shift(off, gdst);
+    qs_shift(off, slot_front);
+    qs_shift(off, slot_row);
+    qs_shift(off, bandptr);
+    qs_shift(off, bandstart);
+  }
 };
 // Schur-complement work item: 64 x 64 tile (ti, tj), ti >= tj, of the update matrix of front `front`
 struct TileItem {

@@ -24,6 +24,7 @@ __device__ __forceinline__ double row_absmax(const Csr& M, int row, double rs, c
 
 __global__ void __launch_bounds__(QS_THREADS)
     k_ruiz_norms(RuizArgs A, double* dx, double* dy, double* dz) {
+  QS_BATCH(A, dx, dy, dz);
   const int N = A.n + A.p + A.m;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     if (i < A.n) {
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(QS_THREADS)
 
 // one scalar per second-order cone: the largest row norm of the cone
 __global__ void __launch_bounds__(QS_THREADS) k_ruiz_cone_max(int nsoc, const int* soc_ptr, double* dz) {
+  QS_BATCH(soc_ptr, dz);
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (k >= nsoc) return;
   const int o = soc_ptr[k], e = soc_ptr[k + 1];
@@ -55,6 +57,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_ruiz_cone_max(int nsoc, const in
 }
 
 __global__ void __launch_bounds__(QS_THREADS) k_ruiz_update(int n, const double* norm, double* scale) {
+  QS_BATCH(norm, scale);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double t = norm[i];
     if (t > 0.0) scale[i] *= 1.0 / sqrt(t);
@@ -62,6 +65,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_ruiz_update(int n, const double*
 }
 
 __global__ void __launch_bounds__(QS_THREADS) k_scale_csr(Csr M, double* val, const double* rs, const double* cs) {
+  QS_BATCH(M, val, rs, cs);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   for (int row = warp; row < M.rows; row += (gridDim.x * blockDim.x) >> 5) {
     const double r = rs[row];
@@ -73,6 +77,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_scale_csr(Csr M, double* val, co
 __global__ void __launch_bounds__(QS_THREADS)
     k_scale_kkt(int n, int p, int m, const i64* Kp, const int* Ki, double* Kx, const double* D, const double* E,
                 const double* F) {
+  QS_BATCH(Kp, Ki, Kx, D, E, F);
   const int N = n + p + m;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   for (int col = warp; col < N; col += (gridDim.x * blockDim.x) >> 5) {
@@ -85,6 +90,7 @@ __global__ void __launch_bounds__(QS_THREADS)
 }
 
 __global__ void __launch_bounds__(QS_THREADS) k_vec_scale(int n, double* v, const double* s, int divide) {
+  QS_BATCH(v, s);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     v[i] = divide ? v[i] / s[i] : v[i] * s[i];
 }
@@ -100,31 +106,31 @@ int vg(i64 n) {
 void qsk_ruiz(const RuizArgs& A, int iters, double* work_x, double* work_y, double* work_z, cudaStream_t st) {
   const i64 N = (i64)A.n + A.p + A.m;
   for (int it = 0; it < iters; ++it) {
-    k_ruiz_norms<<<vg(N), QS_THREADS, 0, st>>>(A, work_x, work_y, work_z);
+    k_ruiz_norms<<<qs_grid(vg(N)), QS_THREADS, 0, st>>>(A, work_x, work_y, work_z);
     if (A.nsoc > 0)
-      k_ruiz_cone_max<<<(A.nsoc * 32 + QS_THREADS - 1) / QS_THREADS, QS_THREADS, 0, st>>>(A.nsoc, A.soc_ptr, work_z);
-    k_ruiz_update<<<vg(A.n), QS_THREADS, 0, st>>>(A.n, work_x, A.D);
-    if (A.p > 0) k_ruiz_update<<<vg(A.p), QS_THREADS, 0, st>>>(A.p, work_y, A.E);
-    k_ruiz_update<<<vg(A.m), QS_THREADS, 0, st>>>(A.m, work_z, A.F);
+      k_ruiz_cone_max<<<qs_grid((A.nsoc * 32 + QS_THREADS - 1) / QS_THREADS), QS_THREADS, 0, st>>>(A.nsoc, A.soc_ptr, work_z);
+    k_ruiz_update<<<qs_grid(vg(A.n)), QS_THREADS, 0, st>>>(A.n, work_x, A.D);
+    if (A.p > 0) k_ruiz_update<<<qs_grid(vg(A.p)), QS_THREADS, 0, st>>>(A.p, work_y, A.E);
+    k_ruiz_update<<<qs_grid(vg(A.m)), QS_THREADS, 0, st>>>(A.m, work_z, A.F);
   }
 }
 
 void qsk_ruiz_apply(const RuizArgs& A, const i64* Kp, const int* Ki, double* Kx, double* c, double* b, double* h,
                     cudaStream_t st) {
   auto sc = [&](const Csr& M, const double* rs, const double* cs) {
-    if (M.rows > 0) k_scale_csr<<<vg((i64)M.rows * 32), QS_THREADS, 0, st>>>(M, const_cast<double*>(M.val), rs, cs);
+    if (M.rows > 0) k_scale_csr<<<qs_grid(vg((i64)M.rows * 32)), QS_THREADS, 0, st>>>(M, const_cast<double*>(M.val), rs, cs);
   };
   sc(A.Pf, A.D, A.D);
   sc(A.At, A.D, A.E);
   sc(A.Gt, A.D, A.F);
   sc(A.Ar, A.E, A.D);
   sc(A.Gr, A.F, A.D);
-  k_scale_kkt<<<vg(((i64)A.n + A.p + A.m) * 32), QS_THREADS, 0, st>>>(A.n, A.p, A.m, Kp, Ki, Kx, A.D, A.E, A.F);
+  k_scale_kkt<<<qs_grid(vg(((i64)A.n + A.p + A.m) * 32)), QS_THREADS, 0, st>>>(A.n, A.p, A.m, Kp, Ki, Kx, A.D, A.E, A.F);
   qsk_vec_scale(A.n, c, A.D, 0, st);
   qsk_vec_scale(A.p, b, A.E, 0, st);
   qsk_vec_scale(A.m, h, A.F, 0, st);
 }
 
 void qsk_vec_scale(int n, double* v, const double* s, int divide, cudaStream_t st) {
-  if (n > 0) k_vec_scale<<<vg(n), QS_THREADS, 0, st>>>(n, v, s, divide);
+  if (n > 0) k_vec_scale<<<qs_grid(vg(n)), QS_THREADS, 0, st>>>(n, v, s, divide);
 }

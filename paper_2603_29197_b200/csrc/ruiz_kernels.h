@@ -7,6 +7,17 @@ struct RuizArgs {
   const int* soc_ptr;
   Csr Pf, At, Gt, Ar, Gr;
   double *D, *E, *F;  // [n], [p], [m]; start at 1
+  __device__ void shift(size_t off) {
+    qs_shift(off, soc_ptr);
+    qs_shift(off, Pf);
+    qs_shift(off, At);
+    qs_shift(off, Gt);
+    qs_shift(off, Ar);
+    qs_shift(off, Gr);
+    qs_shift(off, D);
+    qs_shift(off, E);
+    qs_shift(off, F);
+  }
 };
 
 void qsk_ruiz(const RuizArgs& A, int iters, double* work_x, double* work_y, double* work_z, cudaStream_t st);

@@ -234,6 +234,7 @@ __device__ __forceinline__ RowRange locate1(int tpr, int mode) {
 // r_dual = P x + c + A'y + G'z (ipm.py:76), -r_dual -> rhs[0:n]; |Px|, |A'y|, |G'z|, |r_dual| (inf norms), x'Px, c'x
 template <int MODE>
 __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
+  QS_BATCH(A);
   enum { PX, ATY, GTZ, RD, XPX, CX, NV };
   double v[NV];
 #pragma unroll
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
 // r_eq = A x - b (ipm.py:77), -r_eq -> rhs[n:n+p]; |Ax|, |r_eq|
 template <int MODE>
 __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
+  QS_BATCH(A);
   enum { AX, RE, NV };
   double v[NV] = {0.0, 0.0};
   const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Ar.tpr, MODE);
@@ -327,6 +329,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
 // r_cone = G x + s - h (ipm.py:78); |Gx|, |s|, |r_cone|, gap = s'z (ipm.py:79)
 template <int MODE>
 __global__ void __launch_bounds__(QS_THREADS) k_resid_cone(ResidualArgs A) {
+  QS_BATCH(A);
   enum { GX, SN, RC, GAP, NV };
   double v[NV] = {0.0, 0.0, 0.0, 0.0};
   const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Gr.tpr, MODE);
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_cone(ResidualArgs A) {
 // product runs over the stored entries of K; same operator, other rounding).
 __global__ void __launch_bounds__(QS_THREADS)
     k_kkt_residual(KktResidualArgs A, int nbd, int nbe, int nbc) {
+  QS_BATCH(A);
   double v[1] = {0.0};
   const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
   const double* vx = A.v;
@@ -480,6 +484,7 @@ __global__ void __launch_bounds__(QS_THREADS)
 
 // plain y (+)= M x, gather form
 __global__ void __launch_bounds__(QS_THREADS) k_spmv_csr(Csr M, const double* x, double* y, int accumulate) {
+  QS_BATCH(M, x, y);
   if (M.tpr == QS_TPR_CTA) {
     __shared__ double rsm[QS_THREADS / 32];
     for (int row = blockIdx.x; row < M.rows; row += gridDim.x) {
@@ -499,6 +504,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_spmv_csr(Csr M, const double* x,
 // the operator form.  Scatter side uses fp64 atomics (order not fixed).
 __global__ void __launch_bounds__(QS_THREADS)
     k_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out) {
+  QS_BATCH(cp, ri, vx, x, out);
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (col >= ncols) return;
   const double xj = x[col];
@@ -516,17 +522,20 @@ __global__ void __launch_bounds__(QS_THREADS)
 
 __global__ void __launch_bounds__(QS_THREADS) k_axpby(i64 n, double a, const double* x, double b, const double* y,
                                                       double* out) {
+  QS_BATCH(x, y, out);
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
     out[i] = a * x[i] + (y ? b * y[i] : 0.0);
 }
 
 __global__ void __launch_bounds__(QS_THREADS) k_gather(i64 n, const double* __restrict__ src,
                                                        const int* __restrict__ map, double* __restrict__ dst) {
+  QS_BATCH(src, map, dst);
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) dst[i] = src[map[i]];
 }
 
 __global__ void __launch_bounds__(QS_THREADS) k_absmax(i64 n, const double* x, double* out, double* nonfinite,
                                                        GridRed gr) {
+  QS_BATCH(x, out, nonfinite, gr);
   double v[1] = {0.0};
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
     v[0] = absmax(v[0], x[i]);
@@ -578,49 +587,49 @@ int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
   int launches = 0;
   if (A.p > 0) {  // rows of A are the long ones when A is a design matrix: start them first
     const int t = A.Ar.tpr;
-    if (t == 1) k_resid_eq<MODE_THREAD><<<tgrid(A.p), QS_THREADS, 0, st>>>(A);
-    else if (t == QS_TPR_CTA) k_resid_eq<MODE_CTA><<<blocks_for(A.p, t), QS_THREADS, 0, st>>>(A);
-    else k_resid_eq<MODE_GROUP><<<blocks_capped(A.p, t), QS_THREADS, 0, st>>>(A);
+    if (t == 1) k_resid_eq<MODE_THREAD><<<qs_grid(tgrid(A.p)), QS_THREADS, 0, st>>>(A);
+    else if (t == QS_TPR_CTA) k_resid_eq<MODE_CTA><<<qs_grid(blocks_for(A.p, t)), QS_THREADS, 0, st>>>(A);
+    else k_resid_eq<MODE_GROUP><<<qs_grid(blocks_capped(A.p, t)), QS_THREADS, 0, st>>>(A);
     ++launches;
   }
-  if (A.Pf.tpr == 1) k_resid_dual<MODE_THREAD><<<tgrid(A.n), QS_THREADS, 0, st>>>(A);
-  else k_resid_dual<MODE_GROUP><<<blocks_capped(A.n, A.Pf.tpr, 2), QS_THREADS, 0, st>>>(A);
+  if (A.Pf.tpr == 1) k_resid_dual<MODE_THREAD><<<qs_grid(tgrid(A.n)), QS_THREADS, 0, st>>>(A);
+  else k_resid_dual<MODE_GROUP><<<qs_grid(blocks_capped(A.n, A.Pf.tpr, 2)), QS_THREADS, 0, st>>>(A);
   {
     const int t = A.Gr.tpr;
-    if (t == 1) k_resid_cone<MODE_THREAD><<<tgrid(A.m), QS_THREADS, 0, st>>>(A);
-    else if (t == QS_TPR_CTA) k_resid_cone<MODE_CTA><<<blocks_for(A.m, t), QS_THREADS, 0, st>>>(A);
-    else k_resid_cone<MODE_GROUP><<<blocks_capped(A.m, t), QS_THREADS, 0, st>>>(A);
+    if (t == 1) k_resid_cone<MODE_THREAD><<<qs_grid(tgrid(A.m)), QS_THREADS, 0, st>>>(A);
+    else if (t == QS_TPR_CTA) k_resid_cone<MODE_CTA><<<qs_grid(blocks_for(A.m, t)), QS_THREADS, 0, st>>>(A);
+    else k_resid_cone<MODE_GROUP><<<qs_grid(blocks_capped(A.m, t)), QS_THREADS, 0, st>>>(A);
   }
   return launches + 2;
 }
 
 void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st) {
   const int nbd = blocks_capped(A.n, A.Pf.tpr, 2), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
-  k_kkt_residual<<<nbd + nbe + nbc, QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
+  k_kkt_residual<<<qs_grid(nbd + nbe + nbc), QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
 }
 
 void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cudaStream_t st) {
   if (M.rows <= 0) return;
-  k_spmv_csr<<<blocks_for(M.rows, M.tpr), QS_THREADS, 0, st>>>(M, x, y, accumulate);
+  k_spmv_csr<<<qs_grid(blocks_for(M.rows, M.tpr)), QS_THREADS, 0, st>>>(M, x, y, accumulate);
 }
 
 void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out,
                             cudaStream_t st) {
   if (ncols <= 0) return;
   const i64 blocks = ((i64)ncols * 32 + QS_THREADS - 1) / QS_THREADS;
-  k_spmv_sym_upper_csc<<<(unsigned)blocks, QS_THREADS, 0, st>>>(ncols, cp, ri, vx, x, out);
+  k_spmv_sym_upper_csc<<<qs_grid((unsigned)blocks), QS_THREADS, 0, st>>>(ncols, cp, ri, vx, x, out);
 }
 
 void qsk_gather(i64 n, const double* src, const int* map, double* dst, cudaStream_t st) {
   if (n <= 0) return;
-  k_gather<<<vgrid(n), QS_THREADS, 0, st>>>(n, src, map, dst);
+  k_gather<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, src, map, dst);
 }
 
 void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st) {
   if (n <= 0) return;
-  k_axpby<<<vgrid(n), QS_THREADS, 0, st>>>(n, a, x, b, y, out);
+  k_axpby<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, a, x, b, y, out);
 }
 
 void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st) {
-  k_absmax<<<vgrid(n), QS_THREADS, 0, st>>>(n, x, out, nonfinite, gr);
+  k_absmax<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, x, out, nonfinite, gr);
 }

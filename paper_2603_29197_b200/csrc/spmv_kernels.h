@@ -8,6 +8,11 @@ struct Csr {
   const int* idx;
   const double* val;
   int tpr;  // lanes per row (power of two, 1..32)
+  __device__ void shift(size_t off) {
+    qs_shift(off, ptr);
+    qs_shift(off, idx);
+    qs_shift(off, val);
+  }
 };
 
 // compute_residuals (ipm.py:70-103): writes rhs[0:n] = -r_dual, rhs[n:n+p] = -r_eq,
@@ -20,6 +25,11 @@ struct ResidualArgs {
   double* r_cone;
   double* scalars;
   GridRed gr;
+  __device__ void shift(size_t off) {
+    Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), gr.shift(off);
+    qs_shift(off, x), qs_shift(off, y), qs_shift(off, z), qs_shift(off, s), qs_shift(off, c), qs_shift(off, b);
+    qs_shift(off, h), qs_shift(off, rhs), qs_shift(off, r_cone), qs_shift(off, scalars);
+  }
 };
 
 struct KktResidualArgs {
@@ -32,6 +42,10 @@ struct KktResidualArgs {
   double* scalars;
   int slot;            // scalars[slot] = ||r||_inf
   GridRed gr;
+  __device__ void shift(size_t off) {
+    Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), gr.shift(off);
+    qs_shift(off, v), qs_shift(off, rhs), qs_shift(off, w2vz), qs_shift(off, r), qs_shift(off, scalars);
+  }
 };
 
 int qsk_pick_tpr(i64 nnz, i64 rows);
