@@ -205,6 +205,31 @@ int qs_time_kernel(qs_handle* h, int kernel_id, int reps, double* ms_host);
  * pair of events: the cold-cache figure a kernel sees inside a solve */
 int qs_time_kernel_cold(qs_handle* h, int kernel_id, int reps, double* ms_host);
 
+/* ---- Batched small-problem mode (the reference's precedent is its thread-pool sweep over
+ * independent instances, pkg/src/qsocp/bench/runner.py:107-117, pkg/tests/test_api.py:101-118).  `count` instances
+ * with ONE sparsity pattern and cone layout are solved in lockstep on one GPU: every kernel launch carries all
+ * instances (gridDim.z = count), the ordering / symbolic analysis / index maps / launch graphs exist once, and one
+ * host synchronisation per phase serves the whole batch.  Each instance follows exactly the iteration of qs_step /
+ * qs_residuals (same kernels), so its iterates are those of a stand-alone solve.  An instance (all device memory
+ * of one handle) must fit a 32 MiB slot.  A qs_batch is single-threaded like a handle.
+ *   qs_batch_setup       same arguments as qs_setup: the pattern and the numbers of instance 0
+ *   qs_batch_set_values  numbers of ALL instances, each array [count][len] row-major, or NULL (= as at setup)
+ *   qs_batch_solve       status[count] (1 Solved, 2 MaxIters, 3 TimeLimit, 4 NumericalError, 5 NotInterior),
+ *                        iterations[count], x [count][n], y [count][p], z [count][m], s [count][m]
+ *   qs_batch_stats       out4 = {kernel launches, host synchronisations, seconds of the last solve, bytes per slot} */
+typedef struct qs_batch qs_batch;
+qs_batch* qs_batch_create(int device, int64_t count);
+void qs_batch_destroy(qs_batch* bt);
+const char* qs_batch_last_error(qs_batch* bt);
+int qs_batch_setup(qs_batch* bt, int64_t n, int64_t m, int64_t p, int64_t l, int64_t nsoc, const int64_t* q,
+                   const int64_t* Pp, const int64_t* Pi, const double* Px, const int64_t* Ap, const int64_t* Ai,
+                   const double* Ax, const int64_t* Gp, const int64_t* Gi, const double* Gx, const double* c,
+                   const double* b, const double* h, const qs_settings* settings);
+int qs_batch_set_values(qs_batch* bt, const double* Px, const double* Ax, const double* Gx, const double* c,
+                        const double* b, const double* h);
+int qs_batch_solve(qs_batch* bt, int64_t* status, int64_t* iterations, double* x, double* y, double* z, double* s);
+int qs_batch_stats(qs_batch* bt, double* out4);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,6 +72,13 @@ SIGNATURES = {
     "qs_bring_to_interior": (C.c_int, [vp, vp, C.c_double, vp, f64p]),
     "qs_compute_mu": (C.c_int, [vp, vp, vp, f64p]),
     "qs_neg_wtw": (C.c_int, [vp, C.c_int] + [vp] * 7),
+    "qs_batch_create": (vp, [C.c_int, C.c_int64]),
+    "qs_batch_destroy": (None, [vp]),
+    "qs_batch_last_error": (C.c_char_p, [vp]),
+    "qs_batch_setup": (C.c_int, [vp] + [C.c_int64] * 5 + [vp] * 14),
+    "qs_batch_set_values": (C.c_int, [vp] * 7),
+    "qs_batch_solve": (C.c_int, [vp] * 7),
+    "qs_batch_stats": (C.c_int, [vp, vp]),
     "qs_predictor_rhs": (C.c_int, [vp] * 11 + [C.POINTER(C.c_int)]),
     "qs_corrector_rhs": (C.c_int, [vp] * 9 + [C.c_double, C.c_double] + [vp] * 3),
     "qs_post_solve": (C.c_int, [vp] * 8 + [C.c_int, C.c_double, vp, vp, f64p]),

@@ -149,11 +149,27 @@ def solve_batch(make_instance, count: int, settings=None, rank: int = 0, world: 
     return mine, wall
 
 
-def solve_shard(problems, device: int, workers: int = 8):
-    """This rank's share of a batch on GPU `device` -> (records, mode description).  Same-pattern instances keep one
-    handle per worker (analysis, index maps and launch graphs are reused; only the numbers are uploaded)."""
+def solve_shard(problems, device: int, workers: int = 16, max_batch: int = 512):
+    """This rank's share of a batch on GPU `device` -> (records, mode description).
+
+    Same-pattern instances that fit a batch slot go through the lockstep batched mode (batched.py: every launch
+    carries all instances); anything else keeps `workers` instances in flight, one handle + stream each, reusing the
+    pattern where it repeats."""
+    from .batched import same_pattern, solve_batched
     from .problem import Settings
 
+    problems = list(problems)
+    if len(problems) > 1 and all(same_pattern(problems[0], d) for d in problems[1:]):
+        try:
+            t0 = time.perf_counter()
+            res = solve_batched(problems, Settings(device=device), max_batch)
+            dt = time.perf_counter() - t0
+            recs = [InstanceRecord(i, 0, r.status.value, int(r.iterations), float(r.objective), float(r.setup_seconds),
+                                   float(r.solve_seconds)) for i, r in enumerate(res)]
+            return recs, (f"lockstep batches of {min(max_batch, len(problems))} instances per launch "
+                          f"(qs_batch_*), {dt / len(problems) * 1e3:.3f} ms per instance")
+        except MemoryError:
+            pass  # an instance does not fit a slot: per-instance handles below
     fn = pattern_reuse_solver()
     recs, _ = solve_batch(lambda i: problems[i], len(problems), Settings(device=device), solve_fn=fn, workers=workers,
                           device=device)

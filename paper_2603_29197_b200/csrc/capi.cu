@@ -18,19 +18,37 @@
 #include "ruiz_kernels.h"
 #include "spmv_kernels.h"
 
+thread_local int qs_tls_batch = 1;  // common.cuh: instances per launch of this thread (qs_batch_* calls raise it)
+
 // ------------------------------------------------------------ device memory (devmem.h)
 namespace {
+// Batched mode: while a thread works on a batch, every device allocation is a bump allocation inside slot 0 of the
+// batch's arena (so that the whole handle has the same layout in every slot); frees of arena pointers are no-ops.
+struct QsArena {
+  char* base = nullptr;
+  size_t slot_bytes = 0, used = 0;
+  int slots = 0;
+};
+thread_local QsArena* qs_tls_arena = nullptr;
 struct DevMem {
   std::mutex mu;
   bool ready[64] = {false};
   bool pooled[64] = {false};
   cudaStream_t stream[64] = {nullptr};
   std::unordered_set<void*> from_pool;  // pointers handed out by cudaMallocAsync
+  std::vector<std::pair<char*, size_t>> arenas;  // live batch arenas (base, total bytes)
 };
 DevMem g_devmem;
 }  // namespace
 
 cudaError_t qs_dev_malloc(void** p, size_t bytes) {
+  if (QsArena* a = qs_tls_arena) {
+    const size_t at = (a->used + 255) & ~size_t(255);
+    if (at + bytes > a->slot_bytes) return cudaErrorMemoryAllocation;  // the instance does not fit one slot
+    *p = a->base + at;
+    a->used = at + bytes;
+    return cudaSuccess;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return cudaMalloc(p, bytes);
@@ -74,6 +92,8 @@ void qs_dev_free(void* p) {
   bool pooled = false;
   {
     std::lock_guard<std::mutex> lk(g_devmem.mu);
+    for (const auto& a : g_devmem.arenas)
+      if ((char*)p >= a.first && (char*)p < a.first + a.second) return;  // lives and dies with its batch arena
     pooled = g_devmem.from_pool.erase(p) > 0;
   }
   int dev = 0;
@@ -304,8 +324,8 @@ i64 flags_of(const double* sc) {
 
 void clear_flags(qs_handle* h) {
   // SC_FLAG_NOT_INTERIOR .. SC_FLAG_BAD_STEP are contiguous
-  cudaMemsetAsync(h->scalars + SC_FLAG_NOT_INTERIOR, 0, 3 * sizeof(double), h->stream);
-  cudaMemsetAsync(h->scalars + SC_PIVOT_BUMPS, 0, 2 * sizeof(double), h->stream);
+  qs_memset_b(h->scalars + SC_FLAG_NOT_INTERIOR, 0, 3 * sizeof(double), h->stream);
+  qs_memset_b(h->scalars + SC_PIVOT_BUMPS, 0, 2 * sizeof(double), h->stream);
 }
 
 template <class T>
@@ -1647,6 +1667,469 @@ static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, dou
   cudaEventDestroy(b);
   if (ms_host) *ms_host = (double)ms / reps;
   return check_launch(h, "time_kernel");
+}
+
+// ===================================================== batched small-problem mode ======
+// B instances with ONE sparsity pattern, solved in lockstep: every launch of the ordinary solver carries
+// gridDim.z = B (common.cuh), one host synchronisation serves all instances, and the analysis, index maps and
+// launch graphs are built once.  Per-instance decisions (termination, refinement accept / reject, step flags) are
+// taken on the host from the B scalar blocks and handed back as one flag per instance; an instance that has
+// finished keeps its iterate frozen (its share of later launches is wasted work, nothing else).
+}  // extern "C"
+
+struct qs_batch {
+  int device = 0;
+  int B = 0;
+  QsArena arena;
+  qs_handle* h = nullptr;       // the handle of slot 0; every device pointer in it is valid in every slot + b * stride
+  double* sc_host = nullptr;    // pinned [B][SC_COUNT]
+  double* flag_host = nullptr;  // pinned [B]
+  std::vector<double> norm_c, norm_b, norm_h;
+  bool values_dirty = false;
+  std::string err;
+  double solve_seconds = 0.0;
+  i64 launches = 0, syncs = 0;
+};
+
+namespace {
+
+struct BatchScope {
+  explicit BatchScope(qs_batch* b, bool batched_launches = true) {
+    cudaSetDevice(b->device);
+    qs_tls_arena = &b->arena;
+    qs_tls_batch = batched_launches ? b->B : 1;
+  }
+  ~BatchScope() {
+    qs_tls_arena = nullptr;
+    qs_tls_batch = 1;
+  }
+};
+
+int bfail(qs_batch* bt, int code, const std::string& msg) {
+  bt->err = msg;
+  return code;
+}
+
+#define BCK(bt, call)                                                                 \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) return bfail(bt, QS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// all B scalar blocks -> pinned host mirror (one synchronisation for the whole batch)
+int fetch_b(qs_batch* bt) {
+  qs_handle* h = bt->h;
+  BCK(bt, cudaMemcpy2DAsync(bt->sc_host, SC_COUNT * sizeof(double), h->scalars, QS_BSTRIDE, SC_COUNT * sizeof(double),
+                            (size_t)bt->B, cudaMemcpyDeviceToHost, h->stream));
+  BCK(bt, cudaStreamSynchronize(h->stream));
+  h->tm.collect();
+  bt->syncs++;
+  return QS_OK;
+}
+
+// flag_host[b] -> scalars[slot] of instance b
+int upload_flags(qs_batch* bt, int slot) {
+  qs_handle* h = bt->h;
+  BCK(bt, cudaMemcpy2DAsync(h->scalars + slot, QS_BSTRIDE, bt->flag_host, sizeof(double), sizeof(double), (size_t)bt->B,
+                            cudaMemcpyHostToDevice, h->stream));
+  return QS_OK;
+}
+
+inline const double* sc_of(const qs_batch* bt, int b) { return bt->sc_host + (size_t)b * SC_COUNT; }
+
+enum { BS_RUNNING = 0, BS_SOLVED = 1, BS_MAX_ITERS = 2, BS_TIME_LIMIT = 3, BS_NUMERICAL = 4, BS_NOT_INTERIOR = 5 };
+
+// solve_refine (ldl.py:135-166) for every live instance; result in h->xa (= h->sol).  `live` instances whose
+// residual is not finite are marked BS_NUMERICAL.
+int solve_refined_b(qs_batch* bt, const double* rhs, std::vector<int>& status) {
+  qs_handle* h = bt->h;
+  const i64 N = h->N;
+  const int B = bt->B;
+  cudaStream_t st = h->stream;
+  double *x = h->xa, *xn = h->xb, *r = h->ra, *r2 = h->rb;
+  auto backsolve = [&](const double* rr, double* out) {
+    h->tm.begin(T_SOLVE, st);
+    h->ls.solve(rr, out, st);
+    h->tm.end(st);
+    bt->launches += h->ls.launches_per_solve();
+  };
+  auto residual = [&](const double* v, double* rr, int slot) {
+    h->tm.begin(T_REFINE, st);
+    qsk_apply_w2(h->L, h->w, h->eta, h->wbar, v + h->n + h->p, h->w2vz, st);
+    KktResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr,
+                      v,         rhs,       h->w2vz,   rr,    h->scalars, slot, h->gr};
+    qsk_kkt_residual(A, st);
+    h->tm.end(st);
+    bt->launches += 2;
+  };
+  backsolve(rhs, x);
+  h->sol = x;
+  h->n_solve++;
+  if (h->st.refine_iters <= 0) return check_launch(h, "linear solve") ? bfail(bt, QS_E_CUDA, h->err) : QS_OK;
+  qsk_absmax(N, rhs, h->scalars + SC_TMP0, nullptr, h->gr, st);
+  residual(x, r, SC_TMP1);
+  bt->launches += 1;
+  int rc = fetch_b(bt);
+  if (rc) return rc;
+  std::vector<double> stop(B), rn(B);
+  std::vector<char> active(B, 0);
+  int nactive = 0;
+  for (int b = 0; b < B; ++b) {
+    const double* sc = sc_of(bt, b);
+    stop[b] = 1e-12 * (1.0 + sc[SC_TMP0]);  // ldl.py:19,151
+    rn[b] = sc[SC_TMP1];
+    if (status[b] != BS_RUNNING) continue;
+    if (!(fabs(rn[b]) <= DBL_MAX)) {
+      status[b] = BS_NUMERICAL;  // non-finite triangular solve result
+      continue;
+    }
+    active[b] = rn[b] > stop[b];
+    nactive += active[b];
+  }
+  for (i64 it = 0; it < h->st.refine_iters && nactive > 0; ++it) {
+    backsolve(r, h->dx);
+    qsk_axpby(N, 1.0, x, 1.0, h->dx, xn, st);
+    residual(xn, r2, SC_TMP2);
+    bt->launches += 1;
+    rc = fetch_b(bt);
+    if (rc) return rc;
+    nactive = 0;
+    for (int b = 0; b < B; ++b) {
+      bt->flag_host[b] = 0.0;
+      if (!active[b]) continue;
+      const double rn2 = sc_of(bt, b)[SC_TMP2];
+      if (!(fabs(rn2) <= DBL_MAX)) {
+        status[b] = BS_NUMERICAL;  // non-finite refinement residual
+        active[b] = 0;
+      } else if (rn2 >= rn[b]) {
+        active[b] = 0;  // no decrease: keep the previous solution (ldl.py:161-162)
+      } else {
+        bt->flag_host[b] = 1.0;
+        rn[b] = rn2;
+        active[b] = rn2 > stop[b];
+        nactive += active[b];
+      }
+    }
+    rc = upload_flags(bt, SC_TMP3);
+    if (rc) return rc;
+    qsk_copy_if(N, h->scalars + SC_TMP3, xn, x, st);
+    qsk_copy_if(N, h->scalars + SC_TMP3, r2, r, st);
+    bt->launches += 2;
+    // the pinned flags are read by the copy above: do not overwrite them before it ran
+    BCK(bt, cudaStreamSynchronize(st));
+  }
+  return check_launch(h, "linear solve") ? bfail(bt, QS_E_CUDA, h->err) : QS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+qs_batch* qs_batch_create(int device, int64_t count) {
+  int cnt = qs_device_count();
+  if (device < 0 || device >= cnt || count < 1 || count > 65535) {
+    g_error = "qs_batch_create: bad device or instance count (1..65535)";
+    return nullptr;
+  }
+  cudaSetDevice(device);
+  qs_batch* bt = new qs_batch();
+  bt->device = device;
+  bt->B = (int)count;
+  bt->arena.slot_bytes = QS_BSTRIDE;
+  bt->arena.slots = (int)count;
+  const size_t total = (size_t)count * QS_BSTRIDE;
+  if (cudaMalloc((void**)&bt->arena.base, total) != cudaSuccess ||
+      cudaMallocHost((void**)&bt->sc_host, (size_t)count * SC_COUNT * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost((void**)&bt->flag_host, (size_t)count * sizeof(double)) != cudaSuccess) {
+    g_error = std::string("qs_batch_create: ") + cudaGetErrorString(cudaGetLastError());
+    if (bt->arena.base) cudaFree(bt->arena.base);
+    if (bt->sc_host) cudaFreeHost(bt->sc_host);
+    delete bt;
+    return nullptr;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_devmem.mu);
+    g_devmem.arenas.emplace_back(bt->arena.base, total);
+  }
+  {
+    BatchScope sc(bt, false);
+    bt->h = qs_create(device);
+  }
+  if (!bt->h) {
+    qs_batch_destroy(bt);
+    return nullptr;
+  }
+  bt->norm_c.assign(count, 0.0);
+  bt->norm_b.assign(count, 0.0);
+  bt->norm_h.assign(count, 0.0);
+  return bt;
+}
+
+void qs_batch_destroy(qs_batch* bt) {
+  if (!bt) return;
+  cudaSetDevice(bt->device);
+  if (bt->h) {
+    BatchScope sc(bt, false);
+    qs_destroy(bt->h);  // frees of arena pointers are no-ops
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_devmem.mu);
+    auto& v = g_devmem.arenas;
+    v.erase(std::remove_if(v.begin(), v.end(), [&](const std::pair<char*, size_t>& a) { return a.first == bt->arena.base; }),
+            v.end());
+  }
+  cudaFree(bt->arena.base);
+  cudaFreeHost(bt->sc_host);
+  cudaFreeHost(bt->flag_host);
+  delete bt;
+}
+
+const char* qs_batch_last_error(qs_batch* bt) {
+  if (!bt) return g_error.c_str();
+  if (!bt->err.empty()) return bt->err.c_str();
+  return bt->h ? bt->h->err.c_str() : "";
+}
+
+// The shared pattern and the numbers of instance 0 (same arguments as qs_setup); every slot starts as a copy of it.
+int qs_batch_setup(qs_batch* bt, int64_t n, int64_t m, int64_t p, int64_t l, int64_t nsoc, const int64_t* q,
+                   const int64_t* Pp, const int64_t* Pi, const double* Px, const int64_t* Ap, const int64_t* Ai,
+                   const double* Ax, const int64_t* Gp, const int64_t* Gi, const double* Gx, const double* c,
+                   const double* b, const double* hvec, const qs_settings* settings) {
+  if (!bt || !bt->h) return QS_E_INVALID;
+  if (settings && settings->ruiz_iters > 0) return bfail(bt, QS_E_INVALID, "batched mode does not equilibrate");
+  int rc;
+  {
+    BatchScope sc(bt, false);  // slot 0 is set up as an ordinary handle whose memory comes from the arena
+    rc = qs_setup(bt->h, n, m, p, l, nsoc, q, Pp, Pi, Px, Ap, Ai, Ax, Gp, Gi, Gx, c, b, hvec, settings, nullptr);
+  }
+  if (rc) return bfail(bt, rc, bt->h->err.empty() ? "qs_setup failed" : bt->h->err +
+                                  " (batched mode: one instance must fit a 32 MiB slot)");
+  if (!bt->h->pf_map) return bfail(bt, QS_E_INVALID, "batched mode needs the device-assembled KKT path");
+  qs_handle* h = bt->h;
+  // replicate slot 0 (patterns, analysis, values of instance 0, zeroed scratch) into every slot
+  qsk_broadcast((i64)((bt->arena.used + 7) / 8), bt->arena.base, bt->B, h->stream);
+  BCK(bt, cudaStreamSynchronize(h->stream));
+  for (int k = 0; k < bt->B; ++k) {
+    bt->norm_c[k] = h->norm_c;
+    bt->norm_b[k] = h->norm_b;
+    bt->norm_h[k] = h->norm_h;
+  }
+  bt->values_dirty = false;
+  return QS_OK;
+}
+
+// Numbers of all instances at once: each array is [count][len] row-major (len = nnz(P), nnz(A), nnz(G), n, p, m)
+// or null (= every instance keeps the numbers given at setup).
+int qs_batch_set_values(qs_batch* bt, const double* Px, const double* Ax, const double* Gx, const double* c,
+                        const double* b, const double* hvec) {
+  if (!bt || !bt->h || !bt->h->have_problem) return QS_E_INVALID;
+  cudaSetDevice(bt->device);
+  qs_handle* h = bt->h;
+  cudaStream_t st = h->stream;
+  const size_t B = (size_t)bt->B;
+  auto up = [&](const double* src, const double* dst, i64 len) -> cudaError_t {
+    if (!src || len <= 0) return cudaSuccess;
+    h->h2d_extra += (i64)B * len * (i64)sizeof(double);
+    return cudaMemcpy2DAsync(const_cast<double*>(dst), QS_BSTRIDE, src, len * sizeof(double), len * sizeof(double), B,
+                             cudaMemcpyHostToDevice, st);
+  };
+  BCK(bt, up(Px, h->Pu.val, h->nnzP));
+  BCK(bt, up(Ax, h->At.val, h->nnzA));
+  BCK(bt, up(Gx, h->Gt.val, h->nnzG));
+  BCK(bt, up(c, h->c, h->n));
+  BCK(bt, up(b, h->b, h->p));
+  BCK(bt, up(hvec, h->hv, h->m));
+  for (size_t k = 0; k < B; ++k) {
+    if (c) bt->norm_c[k] = inf_norm(c + k * h->n, h->n);
+    if (b) bt->norm_b[k] = inf_norm(b + k * h->p, h->p);
+    if (hvec) bt->norm_h[k] = inf_norm(hvec + k * h->m, h->m);
+  }
+  if (Px || Ax || Gx) bt->values_dirty = true;
+  BCK(bt, cudaStreamSynchronize(st));  // the caller's buffers may be released on return
+  return QS_OK;
+}
+
+// Lockstep interior-point solve of every instance (the loop of ipm.py:259-297 per instance).  Outputs, all [count]
+// or [count][len]: status (1 Solved, 2 MaxIters, 3 TimeLimit, 4 NumericalError, 5 NotInterior), iterations, and the
+// final iterates x [n], y [p], z [m], s [m].
+int qs_batch_solve(qs_batch* bt, int64_t* status_out, int64_t* iterations_out, double* x, double* y, double* z,
+                   double* s) {
+  if (!bt || !bt->h || !bt->h->have_problem) return QS_E_INVALID;
+  BatchScope scope(bt);
+  qs_handle* h = bt->h;
+  cudaStream_t st = h->stream;
+  const int B = bt->B;
+  const i64 n = h->n, p = h->p, m = h->m, N = h->N;
+  const ConeLayout& L = h->L;
+  const auto t_begin = std::chrono::steady_clock::now();
+  auto elapsed = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count(); };
+  int rc;
+#define BRC(call)                                                          \
+  do {                                                                     \
+    rc = (call);                                                           \
+    if (rc) return bt->err.empty() ? bfail(bt, rc, h->err) : rc;           \
+  } while (0)
+  if (bt->values_dirty) {  // row views and KKT values of every instance from its raw numbers (qs_update_values)
+    qsk_gather(h->nnzPf, h->Pu.val, h->pf_map, const_cast<double*>(h->Pf.val), st);
+    qsk_gather(h->nnzA, h->At.val, h->ar_map, const_cast<double*>(h->Ar.val), st);
+    qsk_gather(h->nnzG, h->Gt.val, h->gr_map, const_cast<double*>(h->Gr.val), st);
+    WtwPlan plan = h->wp;
+    plan.slot_start = h->d_slot_start;
+    qsk_kkt_fill(plan, (int)n, (int)p, h->Pu, h->Ar, h->Gr, h->d_Kp, h->d_Ki, h->d_Kx, h->d_pos, st);
+    bt->launches += 4;
+    bt->values_dirty = false;
+  }
+  std::vector<int> status(B, BS_RUNNING), iters(B, 0), stalls(B, 0);
+  // ---- initialize_iterate (ipm.py:135-156)
+  clear_flags(h);
+  {
+    // identity_scaling (cones.py:146-156) written to slot 0, then copied to every slot
+    std::vector<double> one(std::max<i64>(std::max<i64>(L.l, L.nsoc), 1), 1.0), e(m, 0.0);
+    for (int k = 0; k < L.nsoc; ++k) e[h->soc_ptr_host[k]] = 1.0;
+    BCK(bt, cudaMemcpyAsync(h->w, one.data(), L.l * sizeof(double), cudaMemcpyHostToDevice, st));
+    BCK(bt, cudaMemcpyAsync(h->eta, one.data(), L.nsoc * sizeof(double), cudaMemcpyHostToDevice, st));
+    BCK(bt, cudaMemcpyAsync(h->wbar, e.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
+    BCK(bt, cudaStreamSynchronize(st));  // `e` is rewritten below
+    for (int i = 0; i < L.l; ++i) e[i] = 1.0;
+    BCK(bt, cudaMemcpyAsync(h->lam, e.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
+    qsk_broadcast(L.l, h->w, B, st);
+    qsk_broadcast(L.nsoc, h->eta, B, st);
+    qsk_broadcast(m, h->wbar, B, st);
+    qsk_broadcast(m, h->lam, B, st);
+    BCK(bt, cudaStreamSynchronize(st));
+  }
+  BRC(scatter_scaling(h, h->w, h->eta, h->wbar));
+  BRC(do_factor(h));
+  qsk_axpby(n, -1.0, h->c, 0.0, nullptr, h->rhs, st);
+  BCK(bt, qs_copy_b(h->rhs + n, h->b, p * sizeof(double), st));
+  BCK(bt, qs_copy_b(h->rhs + n + p, h->hv, m * sizeof(double), st));
+  BRC(solve_refined_b(bt, h->rhs, status));
+  BCK(bt, qs_copy_b(h->x, h->sol, n * sizeof(double), st));
+  BCK(bt, qs_copy_b(h->y, h->sol + n, p * sizeof(double), st));
+  qsk_axpby(m, -1.0, h->sol + n + p, 0.0, nullptr, h->tmp_m, st);
+  qsk_max_step(L, h->tmp_m, nullptr, h->scalars, -1, SC_SHIFT, h->gr, st);
+  qsk_shift(L, h->tmp_m, h->s, h->scalars, SC_SHIFT, 1.0, st);
+  BCK(bt, qs_memset_b(h->rhs + n, 0, (p + m) * sizeof(double), st));
+  BRC(solve_refined_b(bt, h->rhs, status));
+  qsk_max_step(L, h->sol + n + p, nullptr, h->scalars, -1, SC_SHIFT, h->gr, st);
+  qsk_shift(L, h->sol + n + p, h->z, h->scalars, SC_SHIFT, 1.0, st);
+  qsk_dot((int)m, h->s, h->z, 1.0 / h->deg, h->scalars + SC_MU, h->gr, st);
+  bt->launches += 8;
+  BRC(fetch_b(bt));
+  for (int b = 0; b < B; ++b) {
+    const double* sc = sc_of(bt, b);
+    if (status[b] == BS_RUNNING && (!(fabs(sc[SC_MU]) <= DBL_MAX) || sc[SC_PIVOT_NONFINITE] != 0.0))
+      status[b] = BS_NUMERICAL;
+  }
+  // ---- the loop
+  const double ea = h->st.eps_abs, er = h->st.eps_rel;
+  for (;;) {
+    // compute_residuals (ipm.py:70-103) + check_termination (ipm.py:106-119)
+    h->tm.begin(T_RESID, st);
+    ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->x, h->y, h->z, h->s,
+                   h->c,   h->b,   h->hv,  h->rhs, h->r_cone, h->scalars, h->gr};
+    bt->launches += qsk_residuals(A, st);
+    h->tm.end(st);
+    BRC(fetch_b(bt));
+    int running = 0;
+    const bool out_of_time = elapsed() > h->st.time_limit_seconds;
+    for (int b = 0; b < B; ++b) {
+      if (status[b] != BS_RUNNING) continue;
+      const double* sc = sc_of(bt, b);
+      if (sc[SC_FLAG_NONFINITE] != 0.0) {
+        status[b] = BS_NUMERICAL;
+        continue;
+      }
+      const bool dual_ok = sc[SC_NORM_RDUAL] <=
+                           ea + er * std::max(std::max(sc[SC_NORM_PX], sc[SC_NORM_ATY]), std::max(sc[SC_NORM_GTZ], bt->norm_c[b]));
+      const bool eq_ok = sc[SC_NORM_REQ] <= ea + er * std::max(sc[SC_NORM_AX], bt->norm_b[b]);
+      const bool cone_ok = sc[SC_NORM_RCONE] <= ea + er * std::max(std::max(sc[SC_NORM_GX], sc[SC_NORM_S]), bt->norm_h[b]);
+      const bool gap_ok = sc[SC_GAP] <= ea + er * std::max(fabs(sc[SC_OBJ]), 1.0);
+      if (dual_ok && eq_ok && cone_ok && gap_ok) status[b] = BS_SOLVED;
+      else if (iters[b] >= h->st.max_iters) status[b] = BS_MAX_ITERS;
+      else if (out_of_time) status[b] = BS_TIME_LIMIT;
+      else ++running;
+    }
+    if (running == 0) break;
+    // ---- ipm_step (ipm.py:159-235) for every instance; finished ones keep their iterate
+    clear_flags(h);
+    h->tm.begin(T_CONE, st);
+    qsk_nt_scaling(L, h->s, h->z, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->wp.c4, h->wp.e2, h->r_cone, h->d,
+                   h->rhs + n + p, h->scalars, st);
+    h->tm.end(st);
+    BRC(scatter_scaling(h, h->w, h->eta, h->wbar, /*have_consts=*/L.nsoc > 0));
+    BRC(do_factor(h));
+    BRC(solve_refined_b(bt, h->rhs, status));
+    h->tm.begin(T_CONE, st);
+    qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, h->wdz, h->ds, h->scalars, 0,
+                   h->st.step_fraction, h->deg, h->gr, st);
+    qsk_corrector_rhs(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->ds, h->wdz, h->r_cone, nullptr, h->d,
+                      h->rhs + n + p, h->scalars, st);
+    h->tm.end(st);
+    BRC(solve_refined_b(bt, h->rhs, status));
+    h->tm.begin(T_CONE, st);
+    qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, nullptr, h->ds, h->scalars, 1,
+                   h->st.step_fraction, h->deg, h->gr, st);
+    qsk_update_iterate((int)n, (int)p, (int)m, h->x, h->y, h->z, h->s, h->x2, h->y2, h->z2, h->s2, h->sol, h->ds, h->deg,
+                       h->scalars, h->gr, st);
+    h->tm.end(st);
+    bt->launches += 5;
+    BRC(fetch_b(bt));
+    for (int b = 0; b < B; ++b) {
+      bt->flag_host[b] = 0.0;
+      if (status[b] != BS_RUNNING) continue;
+      const double* sc = sc_of(bt, b);
+      const i64 fl = flags_of(sc);
+      if (fl) {  // the step raised: the last good iterate stays (ipm.py:219-235,292-293)
+        status[b] = (fl & 1) ? BS_NOT_INTERIOR : BS_NUMERICAL;
+        continue;
+      }
+      bt->flag_host[b] = 1.0;
+      iters[b]++;
+      if (sc[SC_ALPHA] < 1e-10) {  // TINY_STEP, MAX_CONSECUTIVE_STALLS (ipm.py:24-25,287-291)
+        if (++stalls[b] >= 3) status[b] = BS_NUMERICAL;
+      } else {
+        stalls[b] = 0;
+      }
+    }
+    BRC(upload_flags(bt, SC_TMP3));
+    qsk_copy_if(n, h->scalars + SC_TMP3, h->x2, h->x, st);
+    qsk_copy_if(p, h->scalars + SC_TMP3, h->y2, h->y, st);
+    qsk_copy_if(m, h->scalars + SC_TMP3, h->z2, h->z, st);
+    qsk_copy_if(m, h->scalars + SC_TMP3, h->s2, h->s, st);
+    bt->launches += 4;
+    BCK(bt, cudaStreamSynchronize(st));  // flag_host is rewritten by the next refinement round
+  }
+  // ---- results
+  auto down = [&](double* dst, const double* src, i64 len) -> cudaError_t {
+    if (!dst || len <= 0) return cudaSuccess;
+    h->d2h_bytes += (i64)B * len * (i64)sizeof(double);
+    return cudaMemcpy2DAsync(dst, len * sizeof(double), src, QS_BSTRIDE, len * sizeof(double), (size_t)B,
+                             cudaMemcpyDeviceToHost, st);
+  };
+  BCK(bt, down(x, h->x, n));
+  BCK(bt, down(y, h->y, p));
+  BCK(bt, down(z, h->z, m));
+  BCK(bt, down(s, h->s, m));
+  BCK(bt, cudaStreamSynchronize(st));
+  for (int b = 0; b < B; ++b) {
+    if (status_out) status_out[b] = status[b];
+    if (iterations_out) iterations_out[b] = iters[b];
+  }
+  bt->solve_seconds = elapsed();
+  (void)N;
+#undef BRC
+  return QS_OK;
+}
+
+// launches issued, host synchronisations, seconds of the last qs_batch_solve, bytes of one slot in use
+int qs_batch_stats(qs_batch* bt, double* out4) {
+  if (!bt || !out4) return QS_E_INVALID;
+  out4[0] = (double)(bt->launches + (bt->h ? bt->h->launches : 0));
+  out4[1] = (double)bt->syncs;
+  out4[2] = bt->solve_seconds;
+  out4[3] = (double)bt->arena.used;
+  return QS_OK;
 }
 
 }  // extern "C"

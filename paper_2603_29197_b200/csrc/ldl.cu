@@ -1062,7 +1062,7 @@ void parallel_ranges(i64 n, Fn fn) {
 template <class... Args>
 void launch_clustered(void (*kern)(Args...), int nfronts, int cl, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nfronts * cl), 1, 1);
+  cfg.gridDim = dim3((unsigned)(nfronts * cl), 1, (unsigned)qs_tls_batch);
   cfg.blockDim = dim3(LDL_THREADS, 1, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
@@ -1476,8 +1476,8 @@ void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
 }
 
 void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t st) {
-  cudaMemsetAsync(L, 0, S.Loff[S.nsup] * 8, st);
-  if (S.Uoff[S.nsup] > 0) cudaMemsetAsync(U, 0, S.Uoff[S.nsup] * 8, st);
+  qs_memset_b(L, 0, S.Loff[S.nsup] * 8, st);
+  if (S.Uoff[S.nsup] > 0) qs_memset_b(U, 0, S.Uoff[S.nsup] * 8, st);
   k_scatter_values<<<qs_grid(grid_for(knnz)), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
   k_add_reg<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, D, reg, L);
   auto leaf_grid = [&](int g) { return (unsigned)(((i64)n_leaf * g + LDL_THREADS - 1) / LDL_THREADS); };

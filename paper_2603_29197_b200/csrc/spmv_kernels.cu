@@ -569,6 +569,20 @@ int vgrid(i64 n) {
   return (int)g;
 }
 
+
+// dst[i] = src[i] where *flag != 0 (the flag is a scalar of the instance: accept / reject decided on the host)
+__global__ void __launch_bounds__(QS_THREADS) k_copy_if(i64 n, const double* flag, const double* src, double* dst) {
+  QS_BATCH(flag, src, dst);
+  if (*flag == 0.0) return;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+// slot z of the batch arena receives the bytes of slot 0 (8-byte words); z = blockIdx.z + 1
+__global__ void __launch_bounds__(QS_THREADS) k_broadcast(i64 nwords, unsigned long long* p) {
+  unsigned long long* dst = (unsigned long long*)((char*)p + (size_t)(blockIdx.z + 1) * QS_BSTRIDE);
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nwords; i += (i64)gridDim.x * blockDim.x) dst[i] = p[i];
+}
+
 }  // namespace
 
 int qsk_pick_tpr(i64 nnz, i64 rows) {
@@ -632,4 +646,13 @@ void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, doub
 
 void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st) {
   k_absmax<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, x, out, nonfinite, gr);
+}
+
+void qsk_copy_if(i64 n, const double* flag, const double* src, double* dst, cudaStream_t st) {
+  if (n > 0) k_copy_if<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, flag, src, dst);
+}
+
+void qsk_broadcast(i64 nwords, void* p, int slots, cudaStream_t st) {
+  if (nwords > 0 && slots > 1)
+    k_broadcast<<<dim3((unsigned)vgrid(nwords), 1, (unsigned)(slots - 1)), QS_THREADS, 0, st>>>(nwords, (unsigned long long*)p);
 }

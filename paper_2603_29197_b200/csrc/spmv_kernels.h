@@ -57,3 +57,6 @@ void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const doubl
 void qsk_gather(i64 n, const double* src, const int* map, double* dst, cudaStream_t st);  // dst[i] = src[map[i]]
 void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st);
 void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st);
+// batched mode (common.cuh): per-instance conditional copy; replication of slot 0's words into the other slots
+void qsk_copy_if(i64 n, const double* flag, const double* src, double* dst, cudaStream_t st);
+void qsk_broadcast(i64 nwords, void* p, int slots, cudaStream_t st);

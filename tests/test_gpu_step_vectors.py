@@ -131,19 +131,31 @@ def test_fused_step_kernels_vs_reference_trace(oracle, name):
         # r_cone from the predictor RHS: rhs_a[n+p:] = -r_cone - W (lam \ -lam_sq)
         d_a = oracle.jordan_divide(sc.lam, -t["lam_sq"], cone)
         r_cone = -(rhs_a[n + p:] + oracle.apply_scaling(sc, d_a))
+        # Near the optimum the cones sit on their boundary: s0^2 - |s1|^2 cancels and |wbar| grows, so a different
+        # summation order moves the results by eps x (condition of the NT scaling), not by eps.  kappa = that
+        # condition at this iterate (1 at the first iterations: the test is tight there, honest later).
+        kappa = 1.0 + float(np.max(np.abs(sc.soc_wbar), initial=0.0)) ** 2
+        for v in (s, z):
+            for k0, q in zip(np.cumsum([cone.orthant_dim, *cone.soc_dims[:-1]]) if cone.soc_dims else [], cone.soc_dims):
+                head, tail = v[k0], v[k0 + 1:k0 + q]
+                kappa = max(kappa, head * head / max(head * head - float(tail @ tail), 1e-300))
+        tol = min(1e-12 * kappa, 1e-6)
         g_sc, g_lsq, g_d, g_rhs = dc.predictor_rhs(s, z, r_cone)
-        assert close(g_sc.lam, sc.lam) and close(g_sc.soc_wbar, sc.soc_wbar) and close(g_lsq, t["lam_sq"])
-        assert close(g_rhs, rhs_a[n + p:], 1e-11)  # r_cone itself was recovered through one rounding
+        assert close(g_sc.lam, sc.lam, tol) and close(g_sc.soc_wbar, sc.soc_wbar, tol) and close(g_lsq, t["lam_sq"], tol)
+        assert close(g_rhs, rhs_a[n + p:], 10 * tol)  # r_cone itself was recovered through one rounding
         wdz_a, g_ds_a, info = dc.post_solve(sc, d_a, t["dz_a"], s, z, corrector=False)
-        assert close(g_ds_a, t["ds_a"], 1e-11)
-        assert rel(info["alpha_aff"], t["info"].alpha_affine)
-        assert abs(info["mu_aff"] - t["info"].mu_affine) <= 1e-9 * max(mu, t["info"].mu_affine)
-        assert abs(info["sigma"] - t["info"].sigma) <= 1e-7 * max(t["info"].sigma, 1e-3)
+        assert close(g_ds_a, t["ds_a"], 10 * tol)
+        assert abs(info["alpha_aff"] - t["info"].alpha_affine) <= max(1e-10, 10 * tol) * t["info"].alpha_affine
+        assert abs(info["mu_aff"] - t["info"].mu_affine) <= max(1e-9, 10 * tol) * max(mu, t["info"].mu_affine)
+        assert abs(info["sigma"] - t["info"].sigma) <= max(1e-7, 100 * tol) * max(t["info"].sigma, 1e-3)
         g_dc, g_d, g_rhs_c = dc.corrector_rhs(sc, t["lam_sq"], t["ds_a"], oracle.apply_scaling(sc, t["dz_a"]), r_cone,
                                               t["info"].sigma, mu)
-        assert close(g_dc, t["d_comp"], 1e-11) and close(g_rhs_c, rhs_c[n + p:], 1e-10)
+        assert close(g_dc, t["d_comp"], 10 * tol) and close(g_rhs_c, rhs_c[n + p:], 100 * tol)
         _, g_ds, info2 = dc.post_solve(sc, oracle.jordan_divide(sc.lam, t["d_comp"], cone), t["dz"], s, z, corrector=True)
-        assert close(g_ds, t["ds"], 1e-10) and rel(info2["alpha"], t["info"].alpha)
+        assert close(g_ds, t["ds"], 100 * tol)
+        assert abs(info2["alpha"] - t["info"].alpha) <= max(1e-10, 100 * tol) * t["info"].alpha
+        if k == 0:
+            assert tol <= 1e-9, "the first iterate is well inside the cone: tight tolerance expected"
         xo, yo, zo, so, mu2, flags = dc.update_iterate(x, y, z, s, np.concatenate([t["dx"], t["dy"], t["dz"]]), t["ds"],
                                                        t["info"].alpha)
         nx, ny, nz, ns, nmu = iterates[k + 1]
