@@ -344,6 +344,8 @@ bool make_csr(qs_handle* h, Csr* M, i64 rows, i64 cols, const i64* ptr, const i6
   M->idx = h->prob_pool.upload(i32.data(), i32.size(), h->stream);
   M->val = h->prob_pool.upload(val, nnz, h->stream);
   M->tpr = qsk_pick_tpr(nnz, rows);
+  M->exact1 = nnz == rows && rows > 0;
+  for (i64 r = 0; r < rows && M->exact1; ++r) M->exact1 = ptr[r] == r;
   cudaStreamSynchronize(h->stream);  // the int32 staging vectors die here
   return M->ptr && M->idx && M->val;
 }
@@ -946,7 +948,7 @@ int qs_spmv_csr(qs_handle* h, int64_t rows, int64_t cols, const int32_t* ptr, co
   int nnz_last = 0;
   CK(h, cudaMemcpyAsync(&nnz_last, ptr + rows, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
-  Csr M{(int)rows, (int)cols, ptr, idx, val, qsk_pick_tpr(nnz_last, rows)};
+  Csr M{(int)rows, (int)cols, ptr, idx, val, qsk_pick_tpr(nnz_last, rows), 0};
   qsk_spmv_csr(M, x, y, accumulate, h->stream);
   h->launches++;
   return check_launch(h, "spmv_csr");

@@ -121,11 +121,15 @@ __device__ __forceinline__ void qs_shift(size_t off, T& x) {
 #define QS_FE_PICK(_1, _2, _3, _4, _5, _6, _7, _8, _9, _10, _11, _12, _13, _14, _15, _16, _17, _18, _19, _20, _21, _22, _23, _24, NAME, ...) NAME
 #define QS_FOR_EACH(m, ...) QS_FE_PICK(__VA_ARGS__, QS_FE_24, QS_FE_23, QS_FE_22, QS_FE_21, QS_FE_20, QS_FE_19, QS_FE_18, QS_FE_17, QS_FE_16, QS_FE_15, QS_FE_14, QS_FE_13, QS_FE_12, QS_FE_11, QS_FE_10, QS_FE_9, QS_FE_8, QS_FE_7, QS_FE_6, QS_FE_5, QS_FE_4, QS_FE_3, QS_FE_2, QS_FE_1)(m, __VA_ARGS__)
 #define QS_MV_(x) x = qs_moved(x, qs_boff_);
+#ifdef QS_NO_BATCH  // A/B builds: the cost of the prologue
+#define QS_BATCH(...)
+#else
 #define QS_BATCH(...)                                               \
   if (gridDim.z > 1 && blockIdx.z > 0) {                            \
     const size_t qs_boff_ = (size_t)blockIdx.z * QS_BSTRIDE;        \
     QS_FOR_EACH(QS_MV_, __VA_ARGS__)                                \
   }
+#endif
 
 // Host side: the batch size of the launches issued by this thread (1 outside qs_batch_* calls).
 extern thread_local int qs_tls_batch;

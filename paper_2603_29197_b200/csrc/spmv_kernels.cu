@@ -81,6 +81,53 @@ __device__ __forceinline__ double row_dot_thread(const Csr& M, int row, const do
   return acc;
 }
 
+// Thread-per-row products with memory-level parallelism: NM matrices x NR rows per thread advance side by side, so
+// the three dependent round trips of a row (row pointer -> index/value -> operand) are paid once per NM * NR rows
+// instead of once per row -- with rows of 1-3 entries the kernel is bound by exactly that latency (ncu: 30 cycles of
+// long-scoreboard stall per issue, 23 % DRAM utilisation with one row at a time).  Entry order within a row is
+// unchanged, so the sums are bitwise those of row_dot_thread.  A matrix whose rows all hold exactly one entry
+// (exact1: a signed permutation such as the G of an epigraph form or of bound constraints) needs no row pointers.
+template <int NM, int NR>
+__device__ __forceinline__ void thread_dots(const Csr* const (&M)[NM], const double* const (&x)[NM],
+                                            const int (&row)[NR], int nrows, double (&acc)[NM][NR]) {
+  int b[NM][NR], len[NM][NR], maxlen = 0;
+#pragma unroll
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const bool ok = row[r] < nrows;
+      if (M[m]->exact1) {
+        b[m][r] = row[r];
+        len[m][r] = ok ? 1 : 0;
+      } else {
+        b[m][r] = ok ? M[m]->ptr[row[r]] : 0;
+        len[m][r] = ok ? M[m]->ptr[row[r] + 1] - b[m][r] : 0;
+      }
+      acc[m][r] = 0.0;
+    }
+#pragma unroll
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) maxlen = max(maxlen, len[m][r]);
+  for (int k = 0; k < maxlen; ++k) {
+    int ix[NM][NR];
+    double va[NM][NR];
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const bool on = k < len[m][r];
+        ix[m][r] = on ? M[m]->idx[b[m][r] + k] : 0;
+        va[m][r] = on ? M[m]->val[b[m][r] + k] : 0.0;
+      }
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (k < len[m][r]) acc[m][r] += va[m][r] * x[m][ix[m][r]];
+  }
+}
+
 // The dual range needs three products per row (P x, A'y, G'z).  Run them side by side: NM matrices x NR rows =
 // NM * NR independent load chains (row pointer -> index/value -> operand) per lane group, so a trip costs three
 // dependent memory round trips instead of nine.
@@ -210,7 +257,7 @@ __device__ __forceinline__ double absmax(double a, double v) {
 // compute_residuals is three launches, one per row range (dual / eq / cone), each compiled for ONE row-product
 // mode: a fused single kernel carried the registers of all nine (range, mode) paths (80 per thread, 3 CTAs per
 // SM) and, with rows this short, the kernel is bound by how many load chains are in flight.
-enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2 };
+enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2, MODE_MLP = 3 };  // MLP: thread per row, several rows in flight
 enum { RANGE_DUAL = 0, RANGE_EQ = 1, RANGE_CONE = 2 };
 
 __device__ __forceinline__ RowRange locate1(int tpr, int mode) {
@@ -232,14 +279,16 @@ __device__ __forceinline__ RowRange locate1(int tpr, int mode) {
 }
 
 // r_dual = P x + c + A'y + G'z (ipm.py:76), -r_dual -> rhs[0:n]; |Px|, |A'y|, |G'z|, |r_dual| (inf norms), x'Px, c'x
-template <int MODE>
+template <int MODE, bool BATCH>
 __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
-  QS_BATCH(A);
+  if (BATCH) {  // moved pointers cost registers (the unmoved ones are read from the parameter bank): own instantiation
+    QS_BATCH(A);
+  }
   enum { PX, ATY, GTZ, RD, XPX, CX, NV };
   double v[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = 0.0;
-  const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Pf.tpr, MODE);
+  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP) ? 1 : A.Pf.tpr, MODE);
   auto finish_row = [&](int row, double px, double aty, double gtz) {
     const double ci = A.c[row], xi = A.x[row];
     const double rd = px + ci + aty + gtz;
@@ -254,6 +303,17 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
   if (MODE == MODE_THREAD) {
     for (int row = r.row; row < A.n; row += r.stride)
       finish_row(row, row_dot_thread(A.Pf, row, A.x), row_dot_thread(A.At, row, A.y), row_dot_thread(A.Gt, row, A.z));
+  } else if (MODE == MODE_MLP) {
+    const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
+    const double* const vecs[3] = {A.x, A.y, A.z};
+    for (int row0 = r.row; row0 < A.n; row0 += 2 * r.stride) {
+      const int rows[2] = {row0, row0 + r.stride};
+      double d[3][2];
+      thread_dots<3, 2>(mats, vecs, rows, A.n, d);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (rows[q] < A.n) finish_row(rows[q], d[0][q], d[1][q], d[2][q]);
+    }
   } else {
     const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
     const double* const vecs[3] = {A.x, A.y, A.z};
@@ -285,12 +345,14 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
 }
 
 // r_eq = A x - b (ipm.py:77), -r_eq -> rhs[n:n+p]; |Ax|, |r_eq|
-template <int MODE>
+template <int MODE, bool BATCH>
 __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
-  QS_BATCH(A);
+  if (BATCH) {  // moved pointers cost registers (the unmoved ones are read from the parameter bank): own instantiation
+    QS_BATCH(A);
+  }
   enum { AX, RE, NV };
   double v[NV] = {0.0, 0.0};
-  const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Ar.tpr, MODE);
+  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP) ? 1 : A.Ar.tpr, MODE);
   auto finish_row = [&](int row, double ax) {
     const double re = ax - A.b[row];
     A.rhs[A.n + row] = -re;
@@ -299,6 +361,17 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
   };
   if (MODE == MODE_THREAD) {
     for (int row = r.row; row < A.p; row += r.stride) finish_row(row, row_dot_thread(A.Ar, row, A.x));
+  } else if (MODE == MODE_MLP) {
+    const Csr* const mats[1] = {&A.Ar};
+    const double* const vecs[1] = {A.x};
+    for (int row0 = r.row; row0 < A.p; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double d[1][4];
+      thread_dots<1, 4>(mats, vecs, rows, A.p, d);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (rows[q] < A.p) finish_row(rows[q], d[0][q]);
+    }
   } else if (MODE == MODE_CTA) {
     __shared__ double rsm[QS_THREADS / 32];
     for (int row = r.row; row < A.p; row += r.stride) {
@@ -327,12 +400,14 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
 }
 
 // r_cone = G x + s - h (ipm.py:78); |Gx|, |s|, |r_cone|, gap = s'z (ipm.py:79)
-template <int MODE>
+template <int MODE, bool BATCH>
 __global__ void __launch_bounds__(QS_THREADS) k_resid_cone(ResidualArgs A) {
-  QS_BATCH(A);
+  if (BATCH) {  // moved pointers cost registers (the unmoved ones are read from the parameter bank): own instantiation
+    QS_BATCH(A);
+  }
   enum { GX, SN, RC, GAP, NV };
   double v[NV] = {0.0, 0.0, 0.0, 0.0};
-  const RowRange r = locate1(MODE == MODE_THREAD ? 1 : A.Gr.tpr, MODE);
+  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP) ? 1 : A.Gr.tpr, MODE);
   auto finish_row = [&](int row, double gx) {
     const double si = A.s[row];
     const double rc = gx + si - A.h[row];
@@ -344,6 +419,33 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_cone(ResidualArgs A) {
   };
   if (MODE == MODE_THREAD) {
     for (int row = r.row; row < A.m; row += r.stride) finish_row(row, row_dot_thread(A.Gr, row, A.x));
+  } else if (MODE == MODE_MLP) {
+    const Csr* const mats[1] = {&A.Gr};
+    const double* const vecs[1] = {A.x};
+    for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      // the row's own operands do not depend on the product: in flight together with the first loads of the chain
+      double si[4], hi[4], zi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = rows[q] < A.m;
+        si[q] = ok ? A.s[rows[q]] : 0.0;
+        hi[q] = ok ? A.h[rows[q]] : 0.0;
+        zi[q] = ok ? A.z[rows[q]] : 0.0;
+      }
+      double d[1][4];
+      thread_dots<1, 4>(mats, vecs, rows, A.m, d);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (rows[q] < A.m) {
+          const double gx = d[0][q], rc = gx + si[q] - hi[q];
+          A.r_cone[rows[q]] = rc;
+          v[GX] = absmax(v[GX], gx);
+          v[SN] = absmax(v[SN], si[q]);
+          v[RC] = absmax(v[RC], rc);
+          v[GAP] += si[q] * zi[q];
+        }
+    }
   } else if (MODE == MODE_CTA) {
     __shared__ double rsm[QS_THREADS / 32];
     for (int row = r.row; row < A.m; row += r.stride) {
@@ -388,11 +490,19 @@ __global__ void __launch_bounds__(QS_THREADS)
   const double* vy = A.v + A.n;
   const double* vz = A.v + A.n + A.p;
   if (r.which == 0 && r.tpr == 1) {
-    for (int row = r.row; row < A.n; row += r.stride) {
-      const double t = A.rhs[row] - (row_dot_thread(A.Pf, row, vx) + row_dot_thread(A.At, row, vy) +
-                                     row_dot_thread(A.Gt, row, vz));
-      A.r[row] = t;
-      v[0] = absmax(v[0], t);
+    const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
+    const double* const vecs[3] = {vx, vy, vz};
+    for (int row0 = r.row; row0 < A.n; row0 += 2 * r.stride) {
+      const int rows[2] = {row0, row0 + r.stride};
+      double d[3][2];
+      thread_dots<3, 2>(mats, vecs, rows, A.n, d);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (rows[q] >= A.n) continue;
+        const double t = A.rhs[rows[q]] - (d[0][q] + d[1][q] + d[2][q]);
+        A.r[rows[q]] = t;
+        v[0] = absmax(v[0], t);
+      }
     }
   } else if (r.which == 0) {
     const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
@@ -454,11 +564,26 @@ __global__ void __launch_bounds__(QS_THREADS)
       }
     }
   } else if (r.tpr == 1) {
-    for (int row = r.row; row < A.m; row += r.stride) {
-      const int i = A.n + A.p + row;
-      const double t = A.rhs[i] - (row_dot_thread(A.Gr, row, vx) - A.w2vz[row]);
-      A.r[i] = t;
-      v[0] = absmax(v[0], t);
+    const Csr* const mats[1] = {&A.Gr};
+    const double* const vecs[1] = {vx};
+    for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
+      const int rows[4] = {row0, row0 + r.stride, row0 + 2 * r.stride, row0 + 3 * r.stride};
+      double rh[4], w2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = rows[q] < A.m;
+        rh[q] = ok ? A.rhs[A.n + A.p + rows[q]] : 0.0;
+        w2[q] = ok ? A.w2vz[rows[q]] : 0.0;
+      }
+      double d[1][4];
+      thread_dots<1, 4>(mats, vecs, rows, A.m, d);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (rows[q] >= A.m) continue;
+        const double t = rh[q] - (d[0][q] - w2[q]);
+        A.r[A.n + A.p + rows[q]] = t;
+        v[0] = absmax(v[0], t);
+      }
     }
   } else {
     for (int row0 = r.row; row0 < A.m; row0 += 4 * r.stride) {
@@ -596,24 +721,50 @@ int qsk_pick_tpr(i64 nnz, i64 rows) {
 }
 
 int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
-  // thread-per-row ranges: enough blocks for 2 rows per thread, at most 16 resident-size waves
-  auto tgrid = [](int rows) { return std::max(1, std::min(148 * 16, (rows + 2 * QS_THREADS - 1) / (2 * QS_THREADS))); };
+  // thread-per-row ranges.  MLP variant (QS_RESID_MLP=0 selects the one-row-at-a-time kernels everywhere, =2 the MLP
+  // kernels everywhere): `per` rows per thread and trip, about one trip per thread, at most the CTAs resident at
+  // once.  Measured at C4 (ncu, profiles/r02e_resid_*): cone range 31.7 -> 23.9 us with four rows in flight; the
+  // dual range (three matrices per row) is SLOWER with two rows in flight (62 registers, 4 CTAs per SM: 44.5 ->
+  // 52.7 us), so it keeps one row per thread and trip.
+  static const int mlp_env = getenv("QS_RESID_MLP") ? atoi(getenv("QS_RESID_MLP")) : 1;
+  static const bool mlp = mlp_env != 0;
+  static const bool mlp_dual = mlp_env == 2;
+  auto tgrid = [](int rows, int per) {
+    if (!mlp) return std::max(1, std::min(148 * 16, (rows + 2 * QS_THREADS - 1) / (2 * QS_THREADS)));
+    return std::max(1, std::min(148 * 8, (rows + per * QS_THREADS - 1) / (per * QS_THREADS)));
+  };
+  const bool bt = qs_tls_batch > 1;
+#define QS_RESID(kern, MODE, grid)                                                       \
+  do {                                                                                   \
+    if (bt) kern<MODE, true><<<qs_grid(grid), QS_THREADS, 0, st>>>(A);                   \
+    else kern<MODE, false><<<qs_grid(grid), QS_THREADS, 0, st>>>(A);                     \
+  } while (0)
+#define QS_RESID_T(kern, rows, per)                                                      \
+  do {                                                                                   \
+    if (mlp) QS_RESID(kern, MODE_MLP, tgrid(rows, per));                                 \
+    else QS_RESID(kern, MODE_THREAD, tgrid(rows, per));                                  \
+  } while (0)
   int launches = 0;
   if (A.p > 0) {  // rows of A are the long ones when A is a design matrix: start them first
     const int t = A.Ar.tpr;
-    if (t == 1) k_resid_eq<MODE_THREAD><<<qs_grid(tgrid(A.p)), QS_THREADS, 0, st>>>(A);
-    else if (t == QS_TPR_CTA) k_resid_eq<MODE_CTA><<<qs_grid(blocks_for(A.p, t)), QS_THREADS, 0, st>>>(A);
-    else k_resid_eq<MODE_GROUP><<<qs_grid(blocks_capped(A.p, t)), QS_THREADS, 0, st>>>(A);
+    if (t == 1) QS_RESID_T(k_resid_eq, A.p, 4);
+    else if (t == QS_TPR_CTA) QS_RESID(k_resid_eq, MODE_CTA, blocks_for(A.p, t));
+    else QS_RESID(k_resid_eq, MODE_GROUP, blocks_capped(A.p, t));
     ++launches;
   }
-  if (A.Pf.tpr == 1) k_resid_dual<MODE_THREAD><<<qs_grid(tgrid(A.n)), QS_THREADS, 0, st>>>(A);
-  else k_resid_dual<MODE_GROUP><<<qs_grid(blocks_capped(A.n, A.Pf.tpr, 2)), QS_THREADS, 0, st>>>(A);
+  if (A.Pf.tpr == 1) {
+    if (mlp_dual) QS_RESID(k_resid_dual, MODE_MLP, tgrid(A.n, 2));
+    else QS_RESID(k_resid_dual, MODE_THREAD, std::max(1, std::min(148 * 16, (A.n + 2 * QS_THREADS - 1) / (2 * QS_THREADS))));
+  }
+  else QS_RESID(k_resid_dual, MODE_GROUP, blocks_capped(A.n, A.Pf.tpr, 2));
   {
     const int t = A.Gr.tpr;
-    if (t == 1) k_resid_cone<MODE_THREAD><<<qs_grid(tgrid(A.m)), QS_THREADS, 0, st>>>(A);
-    else if (t == QS_TPR_CTA) k_resid_cone<MODE_CTA><<<qs_grid(blocks_for(A.m, t)), QS_THREADS, 0, st>>>(A);
-    else k_resid_cone<MODE_GROUP><<<qs_grid(blocks_capped(A.m, t)), QS_THREADS, 0, st>>>(A);
+    if (t == 1) QS_RESID_T(k_resid_cone, A.m, 4);
+    else if (t == QS_TPR_CTA) QS_RESID(k_resid_cone, MODE_CTA, blocks_for(A.m, t));
+    else QS_RESID(k_resid_cone, MODE_GROUP, blocks_capped(A.m, t));
   }
+#undef QS_RESID_T
+#undef QS_RESID
   return launches + 2;
 }
 

@@ -8,6 +8,7 @@ struct Csr {
   const int* idx;
   const double* val;
   int tpr;  // lanes per row (power of two, 1..32)
+  int exact1;  // every row holds exactly one entry (ptr[r] == r): the thread-per-row products skip the row pointers
   __device__ void shift(size_t off) {
     qs_shift(off, ptr);
     qs_shift(off, idx);
