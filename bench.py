@@ -57,6 +57,7 @@ WORKLOADS = {
     # name -> (config key, kwargs of the full workload)
     "C4_group_lasso": ("C4_group_lasso", dict(groups=10_000, qlo=20, qhi=250, samples=2_000, nnz_per_col=3)),
     "C2_lasso": ("C2_lasso", dict(features=100_000, samples=5_000)),
+    "C2_lasso_20k": ("C2_lasso", dict(features=100_000, samples=20_000)),  # SURVEY 8(d)'s C2 as written
     "C3_portfolio": ("C3_portfolio", dict(assets=100_000, factors=100, sector=100)),
     "C1_random_qp": ("C1_random_qp", dict(n=2000, p=500, m=4000)),
     "C5_mpc": ("C5_mpc", dict(horizon=50, nx=12, nu=4)),
@@ -69,6 +70,7 @@ LADDERS = {
                        ("1/32", dict(groups=316, qlo=20, qhi=250, samples=63, nnz_per_col=3)),
                        ("1/10", dict(groups=1000, qlo=20, qhi=250, samples=200, nnz_per_col=3))],
     "C2_lasso": [("1/100", dict(features=1_000, samples=50)), ("1/10", dict(features=10_000, samples=500))],
+    "C2_lasso_20k": [("1/100", dict(features=1_000, samples=200)), ("1/10", dict(features=10_000, samples=2_000))],
     "C3_portfolio": [("1/100", dict(assets=1_000, factors=100, sector=100)),
                      ("1/10", dict(assets=10_000, factors=100, sector=100))],
     "C1_random_qp": [("1/4", dict(n=500, p=125, m=1000)), ("1/2", dict(n=1000, p=250, m=2000))],
@@ -448,6 +450,19 @@ def run_ours(args):
 
             orc.build()
         ladder = gpu_ladder(args.workload, local_rank, args.cpu_budget, not args.no_cpu)
+        full_cpu = offline_record(args.workload, "full")
+        if full_cpu:  # the top rung: this run's own measurement against the committed offline CPU run of the same input
+            top = {"scale": "1/1", "config": full_kw, "kkt_nnz": configs.kkt_nnz(data),
+                   "gpu": {"status": "Solved", "iterations": int(round(iters_per)), "objective": float(res.objective)
+                           if args.e2e_steps > 0 else None, "setup_seconds": e2e_setup, "solve_seconds": per_solve,
+                           "e2e_seconds": e2e_s}, "cpu": full_cpu}
+            top["iterations_equal"] = full_cpu["iterations"] == top["gpu"]["iterations"]
+            if top["gpu"]["objective"] is not None:
+                top["objective_rel_diff"] = abs(full_cpu["objective"] - top["gpu"]["objective"]) / max(1.0, abs(full_cpu["objective"]))
+            top["ratio_solve"] = full_cpu["solve_seconds"] / per_solve
+            if args.e2e_steps > 0:
+                top["ratio_e2e"] = (full_cpu["setup_seconds"] + full_cpu["solve_seconds"]) / e2e_s
+            ladder.append(top)
         live = [r for r in ladder if r.get("cpu", {}).get("source", "").startswith("measured")]
         if live:
             r = live[-1]

@@ -13,10 +13,10 @@ python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 python tests/gpu_microbench.py > $OUT/microbench.txt 2>&1
 # the other BASELINE configurations (parity-size cases, not the headline) and the C5 batch on one GPU
-for w in C1_random_qp C2_lasso C3_portfolio C5_mpc; do
+for w in C1_random_qp C2_lasso C2_lasso_20k C3_portfolio C5_mpc; do
   python bench.py --workload $w --no-batch --cpu-budget 20 > $OUT/bench_$w.json 2> $OUT/bench_$w.err
 done
-python tests/gpu_batch_throughput.py 128 > $OUT/c5_batch_throughput.txt 2>&1
+python tests/gpu_batched_throughput.py 512 > $OUT/c5_batched_throughput.txt 2>&1
 python tests/gpu_factor_profile.py > $OUT/ldl_factor_solve_ms.txt 2>&1
 # the torchrun launch the driver uses for N > 1, here with one rank (NCCL init, barrier, max over ranks)
 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
