@@ -197,6 +197,9 @@ int qs_get_timers(qs_handle* h, double* timers8);
 /* bytes copied host -> device (problem data, KKT column pointers, analysis structures) and device -> host (scalar
  * blocks per phase, the final iterate) by this handle so far */
 int qs_get_transfer_bytes(qs_handle* h, int64_t* h2d, int64_t* d2h);
+/* factor / solve calls of the linear system replayed from a captured CUDA graph vs issued as direct launches
+ * (capture is impossible on the legacy NULL stream and inside a foreign capture) */
+int qs_get_graph_stats(qs_handle* h, int64_t* replays, int64_t* direct);
 int qs_get_factor_stats(qs_handle* h, double* stats8);
 /* time `reps` launches of one hot-path kernel on the current state (CUDA events on the handle's stream);
  * kernel ids in INTEGRATION.md.  Returns mean milliseconds per launch. */

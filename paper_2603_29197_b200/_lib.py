@@ -72,6 +72,7 @@ SIGNATURES = {
     "qs_bring_to_interior": (C.c_int, [vp, vp, C.c_double, vp, f64p]),
     "qs_compute_mu": (C.c_int, [vp, vp, vp, f64p]),
     "qs_neg_wtw": (C.c_int, [vp, C.c_int] + [vp] * 7),
+    "qs_get_graph_stats": (C.c_int, [vp, vp, vp]),
     "qs_batch_create": (vp, [C.c_int, C.c_int64]),
     "qs_batch_destroy": (None, [vp]),
     "qs_batch_last_error": (C.c_char_p, [vp]),

@@ -1564,6 +1564,13 @@ int qs_get_timers(qs_handle* h, double* timers8) {
   return QS_OK;
 }
 
+int qs_get_graph_stats(qs_handle* h, int64_t* replays, int64_t* direct) {
+  if (!h) return QS_E_INVALID;
+  if (replays) *replays = h->ls.graph_counts[0];
+  if (direct) *direct = h->ls.graph_counts[1];
+  return QS_OK;
+}
+
 int qs_get_factor_stats(qs_handle* h, double* s8) {
   NEED_PROBLEM(h)
   const Symbolic& S = h->ls.S;

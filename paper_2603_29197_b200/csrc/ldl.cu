@@ -1435,13 +1435,15 @@ namespace {
 // Replay the launches of `body` from a graph captured on first use for the argument pair (a, b).
 template <class Body>
 void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const void* a, const void* b, cudaStream_t st,
-                 Body body) {
+                 long long* counts /*[2]: graph replays, direct launch sequences*/, Body body) {
   if (!enabled) {
+    counts[1]++;
     body();
     return;
   }
   for (const LinSys::GraphEntry& e : cache)
     if (e.a == a && e.b == b) {
+      counts[0]++;
       cudaGraphLaunch(e.exec, st);
       return;
     }
@@ -1450,6 +1452,7 @@ void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const voi
   if (cs != cudaStreamCaptureStatusNone || cache.size() >= 16 ||
       cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     cudaGetLastError();
+    counts[1]++;
     body();  // already inside someone else's capture, too many variants, or capture unavailable
     return;
   }
@@ -1458,9 +1461,11 @@ void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const voi
   cudaGraphExec_t exec = nullptr;
   if (cudaStreamEndCapture(st, &g) == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
     cache.push_back(LinSys::GraphEntry{a, b, exec});
+    counts[0]++;
     cudaGraphLaunch(exec, st);
   } else {
     cudaGetLastError();
+    counts[1]++;
     body();
   }
   if (g) cudaGraphDestroy(g);
@@ -1468,11 +1473,11 @@ void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const voi
 }  // namespace
 
 void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
-  run_graphed(factor_graphs, use_graphs, d_Kx, scalars, st, [&]() { factor_launches(d_Kx, scalars, st); });
+  run_graphed(factor_graphs, use_graphs, d_Kx, scalars, st, graph_counts, [&]() { factor_launches(d_Kx, scalars, st); });
 }
 
 void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
-  run_graphed(solve_graphs, use_graphs, d_rhs, d_sol, st, [&]() { solve_launches(d_rhs, d_sol, st); });
+  run_graphed(solve_graphs, use_graphs, d_rhs, d_sol, st, graph_counts, [&]() { solve_launches(d_rhs, d_sol, st); });
 }
 
 void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t st) {

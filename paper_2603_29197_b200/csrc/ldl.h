@@ -156,6 +156,7 @@ struct LinSys {
   };
   std::vector<GraphEntry> factor_graphs, solve_graphs;
   bool use_graphs = true;
+  long long graph_counts[2] = {0, 0};  // factor / solve calls replayed from a graph, issued as direct launches
   // narrow-level chains: chain_end[lv] > lv + 1 when levels [lv, chain_end[lv]) are fused into one single-CTA launch
   std::vector<int> chain_end, chain_start_of_end;
   int* d_smallptr = nullptr;

@@ -217,6 +217,12 @@ class DeviceSolver:
                 "direct_map")
         return dict(zip(keys, t.tolist()))
 
+    def graph_stats(self) -> dict:
+        """Linear-system calls replayed from a captured CUDA graph vs issued as direct launches."""
+        a, b = C.c_int64(), C.c_int64()
+        self.lib.qs_get_graph_stats(self.h, C.byref(a), C.byref(b))
+        return {"graph_replays": a.value, "direct_launch_sequences": b.value}
+
     def time_kernel(self, kernel_id: int, reps: int = 20, cold: bool = False) -> float:
         """Mean milliseconds per launch of one hot-path kernel (CUDA events on the handle's stream).  cold=True
         flushes the L2 before every timed launch (the figure the kernel sees inside a solve)."""
