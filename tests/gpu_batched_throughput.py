@@ -35,6 +35,34 @@ def main(count=512):
         print(f"lockstep batch of {size:4d}: {count / dt:9.1f} instances/s  ({dt / count * 1e3:.3f} ms per instance, "
               f"setup {t_setup:.2f} s once, mean iterations {sum(r.iterations for r in res) / count:.2f}, "
               f"device seconds per batch {st['solve_seconds']:.4f}, slot {st['slot_bytes'] / 2**20:.2f} MiB)", flush=True)
+    # several lockstep batches side by side (own arena + stream each, one host thread each): the synchronisation gaps
+    # of one batch are filled by the launches of the others
+    from concurrent.futures import ThreadPoolExecutor
+
+    for nb, size in ((2, 256), (4, 128), (2, 512), (4, 256)):
+        if nb * size > 2 * count:
+            continue
+        solvers = [BatchSolver(probs[0], size) for _ in range(nb)]
+        chunks = [probs[k0:k0 + size] for k0 in range(0, count, size)]
+        reps = max(1, (nb * size) // count)  # enough work for every solver
+        chunks = chunks * reps
+
+        def run(args):
+            bs, mine = args
+            return [r for c in mine for r in bs.solve(c, check_pattern=False)]
+
+        with ThreadPoolExecutor(nb) as pool:
+            list(pool.map(run, [(bs, [chunks[0]]) for bs in solvers]))  # warm-up
+            t = time.perf_counter()
+            res = list(pool.map(run, [(bs, chunks[i::nb]) for i, bs in enumerate(solvers)]))
+            dt = time.perf_counter() - t
+        total = sum(len(r) for r in res)
+        assert all(r.status.value == "Solved" for rr in res for r in rr)
+        for bs in solvers:
+            bs.close()
+        out.setdefault("concurrent_lockstep", {})[f"{nb}x{size}"] = total / dt
+        print(f"{nb} lockstep batches of {size} side by side: {total / dt:9.1f} instances/s  ({total} instances in {dt:.3f} s)",
+              flush=True)
     for workers in (8, 16, 32):
         fn = pattern_reuse_solver()
         n = min(count, 256)

@@ -21,19 +21,23 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
-dominant = sys.argv[2] if len(sys.argv) > 2 else r"k_neg_wtw<2, 1>"
+dominant = sys.argv[2] if len(sys.argv) > 2 else r"k_neg_wtw<2, 1"
 src = os.path.join(ROOT, "gpurun_out", tag)
 dst = os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)
 
 for name in ("bench.json", "bench_reference.json", "microbench.txt", "pytest_gpu.log", "smoke.log", "gpu.txt",
              "bench_torchrun1.json", "bench_C1_random_qp.json", "bench_C2_lasso.json", "bench_C3_portfolio.json",
-             "bench_C5_mpc.json", "c5_batch_throughput.txt", "ldl_factor_solve_ms.txt"):
+             "bench_C5_mpc.json", "bench_C2_lasso_20k.json", "c5_batch_throughput.txt", "c5_batched_throughput.txt",
+             "ldl_factor_solve_ms.txt"):
     p = os.path.join(src, name)
     if os.path.exists(p) and os.path.getsize(p) > 0:
         shutil.copy(p, os.path.join(dst, f"{tag}_{name}"))
 
 lp = os.path.join(src, "launches.csv")
+if not os.path.exists(lp) and os.path.exists(lp + ".gz"):  # the round script compresses it on the box
+    with gzip.open(lp + ".gz", "rt") as f, open(lp, "w") as g:
+        g.write(f.read())
 if os.path.exists(lp):
     lines = [ln for ln in open(lp) if ln.startswith('"')]
     rd = csv.reader(lines)
@@ -55,8 +59,10 @@ if os.path.exists(lp):
         f.writelines(lines)
 
 rep = os.path.join(src, "hot_kernels.ncu-rep")
-if os.path.exists(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rawcsv = os.path.join(src, "hot_kernels_raw.csv")  # exported on the box when the report is too large to travel
+if os.path.exists(rep) or os.path.exists(rawcsv):
+    raw = (open(rawcsv).read() if os.path.exists(rawcsv) else
+           subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
     want = ["Kernel Name", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
@@ -86,4 +92,8 @@ if os.path.exists(rep):
         cur["C4_group_lasso"] = sum(traffic["samples"]) / len(traffic["samples"])
         cur["source"] = f"profiles/{tag}_hot_kernels_ncu.csv ({dominant}, mean of {len(traffic['samples'])} launches, C4 cone layout)"
         json.dump(cur, open(tp, "w"), indent=1)
+for extra in ("hot_kernels_source.csv.gz",):
+    p = os.path.join(src, extra)
+    if os.path.exists(p):
+        shutil.copy(p, os.path.join(dst, f"{tag}_{extra}"))
 print("profiles/ updated from", src)
