@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(LDL_THREADS)
   if (bumps) atomicAdd(&scalars[SC_PIVOT_BUMPS], (double)bumps);
 }
 
-__global__ void __launch_bounds__(LDL_THREADS)
+template <int T, int MINB>
+__global__ void __launch_bounds__(T, MINB)
     k_blk_panel(DevSym S, const int* list, int kb, double* L, const double* Dg) {
   QS_BATCH(S, list, L, Dg);
   const int s = list[blockIdx.y];
@@ -1532,8 +1533,19 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
                                                                                               reg, dyn_eps, scalars);
         const int rows_below = mx_nr - kb - 1;
         if (rows_below > 0) {
-          dim3 gp((rows_below + LDL_THREADS - 1) / LDL_THREADS, nb_fronts);
-          k_blk_panel<<<qs_grid(gp), LDL_THREADS, 0, st>>>(D, lst, kb, L, Dg);
+          // thread-per-row trsm: 144 registers = ONE 256-thread CTA per SM (ncu r02g: 11 % of the warp slots active);
+          // capped at 128 registers (32 bytes of spills) two CTAs fit: 53.4 -> 51.0 ms per C4 factorisation.
+          // QS_PANEL_CFG: 0 = uncapped, 1 = 256 x 2 (default), 2 = 128 x 4, 3 = 128 x 3, 4 = 64 x 8 (all measured)
+          static const int cfg = getenv("QS_PANEL_CFG") ? atoi(getenv("QS_PANEL_CFG")) : 1;
+          const int T = (cfg == 2 || cfg == 3) ? 128 : (cfg == 4 ? 64 : LDL_THREADS);
+          dim3 gp((rows_below + T - 1) / T, nb_fronts);
+          switch (cfg) {
+            case 0: k_blk_panel<256, 1><<<qs_grid(gp), T, 0, st>>>(D, lst, kb, L, Dg); break;
+            case 2: k_blk_panel<128, 4><<<qs_grid(gp), T, 0, st>>>(D, lst, kb, L, Dg); break;
+            case 3: k_blk_panel<128, 3><<<qs_grid(gp), T, 0, st>>>(D, lst, kb, L, Dg); break;
+            case 4: k_blk_panel<64, 8><<<qs_grid(gp), T, 0, st>>>(D, lst, kb, L, Dg); break;
+            default: k_blk_panel<256, 2><<<qs_grid(gp), T, 0, st>>>(D, lst, kb, L, Dg); break;
+          }
         }
         const int cols_left = mx_ns - kb - 1;
         if (!left && cols_left > 0) {
