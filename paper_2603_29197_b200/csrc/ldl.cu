@@ -1178,6 +1178,12 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
     smallptr[lv + 1] = (int)small.size();
     blkptr[lv + 1] = (int)blk.size();
     slabptr[lv + 1] = (int)slabs.size();
+    // widest panels first: the fronts of a chunk (below) then need the same number of block steps
+    std::stable_sort(blk.begin() + blkptr[lv], blk.end(), [&](int a, int b) {
+      const int na = S.col0[a + 1] - S.col0[a], nb = S.col0[b + 1] - S.col0[b];
+      if (na != nb) return na > nb;
+      return (S.rowptr[a + 1] - S.rowptr[a]) > (S.rowptr[b + 1] - S.rowptr[b]);
+    });
   }
   n_leaf = (int)leaf.size();
   leaf_group = 4;
@@ -1203,15 +1209,39 @@ std::string LinSys::analyze(i64 N_, const i64* Kp, const i64* Ki, i64 knnz_full,
   {
     std::vector<TileItem> tiles;
     tileptr.assign(S.nlevels + 1, 0);
+    blk_chunks.clear();
+    chunkptr.assign(S.nlevels + 1, 0);
+    // chunk budget: panel bytes per chunk (QS_LDL_CHUNK_MB; default 0 = one chunk per level).  Measured at C4 (10^4
+    // cone fronts, 4.9 GB of panels): 16 / 32 / 48 / 96 / 200 MB chunks -> 138 / 90 / 76 / 62 / 55 ms per
+    // factorisation against 50.8 ms unchunked -- the lockstep launches need the whole level to fill the machine;
+    // L2 residency of the panels buys less than the extra launch tails cost.
+    const i64 chunk_bytes = (i64)(getenv("QS_LDL_CHUNK_MB") ? atoi(getenv("QS_LDL_CHUNK_MB")) : 0) << 20;
     for (int lv = 0; lv < S.nlevels; ++lv) {
+      BlkChunk c{blkptr[lv], 0, 0, 0, (i64)tiles.size(), 0};
+      i64 bytes = 0;
+      auto close = [&]() {
+        if (c.count == 0) return;
+        c.t1 = (i64)tiles.size();
+        blk_chunks.push_back(c);
+        c = BlkChunk{c.b0 + c.count, 0, 0, 0, (i64)tiles.size(), 0};
+        bytes = 0;
+      };
       for (int k = blkptr[lv]; k < blkptr[lv + 1]; ++k) {
         const int fs = blk[k];
-        const int nu = (int)(S.rowptr[fs + 1] - S.rowptr[fs]) - (S.col0[fs + 1] - S.col0[fs]);
+        const int nsf = S.col0[fs + 1] - S.col0[fs], nrf = (int)(S.rowptr[fs + 1] - S.rowptr[fs]);
+        const int nu = nrf - nsf;
         const int nt = (nu + TS - 1) / TS;
         for (int tj = 0; tj < nt; ++tj)
           for (int ti = tj; ti < nt; ++ti) tiles.push_back(TileItem{fs, (short)ti, (short)tj});
+        c.count++;
+        c.max_ns = std::max(c.max_ns, nsf);
+        c.max_nr = std::max(c.max_nr, nrf);
+        bytes += (i64)nsf * nrf * 8;
+        if (c.count >= 65535 || (chunk_bytes > 0 && bytes >= chunk_bytes)) close();
       }
+      close();
       tileptr[lv + 1] = (i64)tiles.size();
+      chunkptr[lv + 1] = (int)blk_chunks.size();
     }
     d_tiles = upload(tiles, &owned, &device_bytes, st);
     if (!d_tiles) return "cudaMalloc failed for the Schur tile list";
@@ -1515,11 +1545,12 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
     const int cnt = smallptr[lv + 1] - smallptr[lv];
     if (cnt > 0)
       k_front_factor<<<qs_grid(cnt), LDL_THREADS, 0, st>>>(D, d_small + smallptr[lv], L, U, Dg, reg, dyn_eps, scalars);
-    // blocked fronts of this level, in chunks that fit gridDim.y
-    for (int b0 = blkptr[lv]; b0 < blkptr[lv + 1]; b0 += 65535) {
-      const int nb_fronts = std::min(65535, blkptr[lv + 1] - b0);
-      const int* lst = d_blk + b0;
-      const int mx_ns = blk_max_ns[lv], mx_nr = blk_max_nr[lv];
+    // blocked fronts of this level, chunk by chunk (see BlkChunk)
+    for (int ci = chunkptr[lv]; ci < chunkptr[lv + 1]; ++ci) {
+      const BlkChunk& ch = blk_chunks[ci];
+      const int nb_fronts = ch.count;
+      const int* lst = d_blk + ch.b0;
+      const int mx_ns = ch.max_ns, mx_nr = ch.max_nr;
       // many fronts: left-looking (each panel block is written once, inner depth kb); a few big fronts:
       // right-looking (rank-32 updates over (ns/64) x (nr/64) tiles keep all SMs busy)
       const bool left = (blkptr[lv + 1] - blkptr[lv]) > 16;
@@ -1554,15 +1585,17 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
           k_blk_update<false><<<qs_grid(gu), LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 0, L, U, Dg);
         }
       }
-    }
-    // Schur complements of the level's blocked fronts: exact tile list
-    const i64 ntile = tileptr[lv + 1] - tileptr[lv];
-    for (i64 t0 = 0; t0 < ntile; t0 += (i64)1 << 30) {
-      const unsigned cnt2 = (unsigned)std::min<i64>((i64)1 << 30, ntile - t0);
-      k_blk_update<true><<<qs_grid(cnt2), LDL_THREADS, 0, st>>>(D, nullptr, d_tiles + tileptr[lv] + t0, 0, 0, L, U, Dg);
+      // Schur complements of the chunk's fronts (exact tile list), while their panels are still in the L2
+      const i64 ntile = ch.t1 - ch.t0;
+      for (i64 t0 = 0; t0 < ntile; t0 += (i64)1 << 30) {
+        const unsigned cnt2 = (unsigned)std::min<i64>((i64)1 << 30, ntile - t0);
+        k_blk_update<true><<<qs_grid(cnt2), LDL_THREADS, 0, st>>>(D, nullptr, d_tiles + ch.t0 + t0, 0, 0, L, U, Dg);
+      }
     }
   }
 }
+
+
 
 void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st) {
   k_permute_in<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, D.perm, d_rhs, xw);
@@ -1653,10 +1686,8 @@ int LinSys::launches_per_factor() const {
       continue;
     }
     k += (slabptr[lv + 1] > slabptr[lv]) + (smallptr[lv + 1] > smallptr[lv]);
-    if (blkptr[lv + 1] > blkptr[lv]) {
-      const int chunks = (blkptr[lv + 1] - blkptr[lv] + 65534) / 65535;
-      k += chunks * (3 * ((blk_max_ns[lv] + NB - 1) / NB) + 1);
-    }
+    for (int ci = chunkptr[lv]; ci < chunkptr[lv + 1]; ++ci)  // update + diag + panel per block step, Schur
+      k += 3 * ((blk_chunks[ci].max_ns + NB - 1) / NB) + 1;
   }
   return k;
 }

@@ -121,6 +121,15 @@ struct LinSys {
   i64* d_poff = nullptr;   // per blocked front: offset into `partial`
   double* partial = nullptr;  // backward-solve row-tile partial sums
   std::vector<int> genptr, slabptr, smallptr, blkptr, blk_max_ns, blk_max_nr, blk_max_nu;
+  // The blocked fronts of a level, sorted by pivot count, are factored chunk by chunk (one chunk per level unless
+  // QS_LDL_CHUNK_MB asks for L2-sized chunks -- measured slower, see ldl.cu); a chunk's launch grids use its own
+  // maxima and its Schur tiles follow its panel steps.
+  struct BlkChunk {
+    int b0, count, max_ns, max_nr;
+    i64 t0, t1;  // range in d_tiles
+  };
+  std::vector<BlkChunk> blk_chunks;
+  std::vector<int> chunkptr;  // [nlevels+1] ranges in blk_chunks
   AsmLists A{};
   EaItem* d_eaitems = nullptr;
   TileItem* d_tiles = nullptr;      // Schur tiles of the blocked fronts, level by level
