@@ -615,6 +615,189 @@ __global__ void __launch_bounds__(LDL_THREADS, 3)
     }
 }
 
+// ---- fused panel factorisation: ONE CTA per front walks all block steps of its panel -----------------------------
+// The lockstep path above launches update / diag / panel once per 32-column step for ALL fronts of a level and
+// re-reads every panel from DRAM at each step (left-looking: columns [0, kb) again and again).  A level with thousands
+// of independent mid-size fronts (the 10^4 cone fronts of C4: ~135 pivots x ~500 rows, 0.5 MB each) does not need the
+// lockstep: a CTA can factor its front from the first to the last step on its own -- the panel stays in the L2 while
+// the CTA works on it, barriers replace launches, and the grid (fronts sorted by size, largest first) balances
+// itself.  MEASURED SLOWER than the lockstep path at C4 (see factor_launches): opt-in, QS_LDL_FUSED=1.  Same arithmetic in the same order as the lockstep kernels (the tile / diagonal / row routines are the
+// same code), so the factor is bitwise the same.  Used for levels with more than QS_FUSED_MIN fronts; a level with a
+// few big fronts (the root) keeps the lockstep / right-looking path, which is what fills the machine there.
+__device__ __forceinline__ void fused_update_tile(const Front& f, const double* Dg, int k_hi, int c_lo, int c_hi, int ti,
+                                                  double (*As)[TSP], double (*Bs)[TSP], double* dsm) {
+  // left-looking: block column [c_lo, c_hi) rows [c_lo + ti * TS, ...) -= L[:, 0:k_hi] D L[c_lo:c_hi, 0:k_hi]'
+  const int i0 = c_lo + ti * TS, j0 = c_lo;
+  const i64 nr = f.nr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wi = 32 * (warp & 1), wj = 16 * (warp >> 1);
+  const int g = lane >> 2, t = lane & 3;
+  const bool live = (i0 + wi < f.nr) && (j0 + wj < c_hi) && (i0 + wi + 31 >= j0 + wj);
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b2 = 0; b2 < 2; ++b2) acc[a][b2][0] = acc[a][b2][1] = 0.0;
+  const int sr = tid & 63, sk = tid >> 6;
+  double ra[8], rb[8], rd = 0.0;
+  auto fetch = [&](int k0) {
+    const int kn = min(NB, k_hi - k0);
+    const int gi = i0 + sr, gj = j0 + sr;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = sk + 4 * u;
+      const bool ka = k < kn && gi < f.nr, kb2 = k < kn && gj < c_hi;
+      ra[u] = ka ? f.Lp[gi + (i64)(k0 + k) * nr] : 0.0;
+      rb[u] = kb2 ? f.Lp[gj + (i64)(k0 + k) * nr] : 0.0;
+    }
+    if (tid < NB) rd = tid < kn ? Dg[f.c0 + k0 + tid] : 0.0;
+  };
+  auto stage = [&]() {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      As[sk + 4 * u][sr] = ra[u];
+      Bs[sk + 4 * u][sr] = rb[u];
+    }
+    if (tid < NB) dsm[tid] = rd;
+  };
+  fetch(0);
+  __syncthreads();  // the previous tile's multiply has finished reading the staging buffers
+  stage();
+  __syncthreads();
+  for (int k0 = 0; k0 < k_hi; k0 += NB) {
+    const bool more = k0 + NB < k_hi;
+    if (more) fetch(k0 + NB);
+    if (live)
+#pragma unroll
+      for (int kk = 0; kk < NB; kk += 4) {
+        double av[4], bv[2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = As[kk + t][wi + 8 * a + g];
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) bv[b2] = Bs[kk + t][wj + 8 * b2 + g] * dsm[kk + t];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2) dmma_8x8x4(acc[a][b2], av[a], bv[b2]);
+      }
+    __syncthreads();
+    if (more) {
+      stage();
+      __syncthreads();
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gj = j0 + wj + 8 * b2 + 2 * t + h;
+      if (gj >= c_hi) continue;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int gi = i0 + wi + 8 * a + g;
+        if (gi >= f.nr || gi < gj) continue;
+        f.Lp[gi + (i64)gj * nr] -= acc[a][b2][h];
+      }
+    }
+}
+
+// 32 x 32 diagonal block by ONE warp (the body of k_blk_diag)
+__device__ __forceinline__ void fused_diag_warp(const Front& f, int kb, double* Dg, const double* reg, double dyn_eps,
+                                                double* scalars) {
+  const int lane = threadIdx.x & 31;
+  const int nb = min(NB, f.ns - kb);
+  const i64 nr = f.nr;
+  double a[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) a[j] = (j <= lane && lane < nb) ? f.Lp[(kb + lane) + (i64)(kb + j) * nr] : 0.0;
+  double dmine = 1.0;
+  int bumps = 0, bad = 0;
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    double d = __shfl_sync(0xffffffffu, a[k], k);
+    if (k < nb) {
+      if (!qs_finite(d)) {
+        bad = 1;
+      } else if (fabs(d) < dyn_eps) {
+        d = (reg[f.c0 + kb + k] >= 0.0) ? dyn_eps : -dyn_eps;
+        bumps += (lane == 0);
+      }
+    } else {
+      d = 1.0;
+    }
+    if (lane == k) dmine = d;
+    const double lik = a[k] / d;
+#pragma unroll
+    for (int j = k + 1; j < NB; ++j) {
+      const double ljk = __shfl_sync(0xffffffffu, lik, j);
+      if (lane >= j) a[j] -= a[k] * ljk;
+    }
+    if (lane > k) a[k] = lik;
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+    if (j < lane && lane < nb) f.Lp[(kb + lane) + (i64)(kb + j) * nr] = a[j];
+  if (lane < nb) {
+    Dg[f.c0 + kb + lane] = dmine;
+    f.Lp[(kb + lane) + (i64)(kb + lane) * nr] = dmine;
+  }
+  if (bad) scalars[SC_PIVOT_NONFINITE] = 1.0;
+  if (bumps) atomicAdd(&scalars[SC_PIVOT_BUMPS], (double)bumps);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(LDL_THREADS, MINB)
+    k_front_blocked(DevSym S, const int* list, double* L, double* Dg, const double* reg, double dyn_eps,
+                    double* scalars) {
+  QS_BATCH(S, list, L, Dg, reg, scalars);
+  const int s = list[blockIdx.x];
+  const Front f = front_of(S, s, L, nullptr);
+  __shared__ double As[NB][TSP];
+  __shared__ double Bs[NB][TSP];
+  __shared__ double dsm[NB];
+  __shared__ double l11[NB][NB + 1];
+  __shared__ double dinv[NB];
+  const int tid = threadIdx.x;
+  const i64 nr = f.nr;
+  for (int kb = 0; kb < f.ns; kb += NB) {
+    const int nb = min(NB, f.ns - kb);
+    if (kb > 0) {
+      const int nti = (f.nr - kb + TS - 1) / TS;
+      for (int ti = 0; ti < nti; ++ti) fused_update_tile(f, Dg, kb, kb, kb + nb, ti, As, Bs, dsm);
+      __syncthreads();  // the updated block column is visible to the whole CTA
+    }
+    if (tid < 32) fused_diag_warp(f, kb, Dg, reg, dyn_eps, scalars);
+    __syncthreads();
+    // rows below the diagonal block: L21 = A21 L11^-T D^-1, a thread per row (the body of k_blk_panel)
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int i = e % nb, j = e / nb;
+      l11[i][j] = (i > j) ? f.Lp[(kb + i) + (i64)(kb + j) * nr] : 0.0;
+    }
+    for (int k = tid; k < nb; k += blockDim.x) dinv[k] = 1.0 / Dg[f.c0 + kb + k];
+    __syncthreads();
+    for (int row = kb + nb + tid; row < f.nr; row += blockDim.x) {
+      double y[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) y[k] = (k < nb) ? f.Lp[row + (i64)(kb + k) * nr] : 0.0;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        if (k < nb) {
+          double acc = y[k];
+#pragma unroll
+          for (int mm = 0; mm < NB; ++mm)
+            if (mm < k) acc -= y[mm] * l11[k][mm];
+          y[k] = acc;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k)
+        if (k < nb) f.Lp[row + (i64)(kb + k) * nr] = y[k] * dinv[k];
+    }
+    __syncthreads();  // the finished block column is visible before the next step reads it
+  }
+}
+
 __global__ void __launch_bounds__(LDL_THREADS) k_zero_cb(DevSym S, const int* list, double* B) {
   QS_BATCH(S, list, B);
   const int s = list[blockIdx.x];
@@ -1554,7 +1737,20 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
       // many fronts: left-looking (each panel block is written once, inner depth kb); a few big fronts:
       // right-looking (rank-32 updates over (ns/64) x (nr/64) tiles keep all SMs busy)
       const bool left = (blkptr[lv + 1] - blkptr[lv]) > 16;
-      for (int kb = 0; kb < mx_ns; kb += NB) {
+      // many independent fronts: one CTA per front can walk all its block steps (k_front_blocked, QS_LDL_FUSED=1;
+      // QS_FUSED_MIN sets the front count from which it is used).  Correct (bitwise the lockstep factor, the solve
+      // tests pass with it) but SLOWER at C4: 58.2 ms per factorisation with two CTAs per SM (128 registers, 888
+      // bytes of spills), 73.7 ms with one, against 50.4 ms for the lockstep launches -- 16 warps per SM with a barrier
+      // after every k-block expose the fetch latency that 10^5-CTA lockstep grids hide.  Kept as an opt-in experiment.
+      static const bool fused_on = getenv("QS_LDL_FUSED") && atoi(getenv("QS_LDL_FUSED")) != 0;
+      static const int fused_min = getenv("QS_FUSED_MIN") ? atoi(getenv("QS_FUSED_MIN")) : 592;
+      const bool fused = fused_on && (blkptr[lv + 1] - blkptr[lv]) >= fused_min;
+      static const int fused_minb = getenv("QS_FUSED_MINB") ? atoi(getenv("QS_FUSED_MINB")) : 2;
+      if (fused && fused_minb == 1)
+        k_front_blocked<1><<<qs_grid(nb_fronts), LDL_THREADS, 0, st>>>(D, lst, L, Dg, reg, dyn_eps, scalars);
+      else if (fused)
+        k_front_blocked<2><<<qs_grid(nb_fronts), LDL_THREADS, 0, st>>>(D, lst, L, Dg, reg, dyn_eps, scalars);
+      for (int kb = 0; kb < mx_ns && !fused; kb += NB) {
         if (left && kb > 0) {  // bring block column kb up to date with the pivots [0, kb)
           const int nti = (mx_nr - kb + TS - 1) / TS;
           dim3 gu(nti, nb_fronts);
