@@ -166,8 +166,8 @@ def solve_shard(problems, device: int, workers: int = 16, max_batch: int = 512):
             dt = time.perf_counter() - t0
             recs = [InstanceRecord(i, 0, r.status.value, int(r.iterations), float(r.objective), float(r.setup_seconds),
                                    float(r.solve_seconds)) for i, r in enumerate(res)]
-            return recs, (f"lockstep batches of {min(max_batch, len(problems))} instances per launch "
-                          f"(qs_batch_*), {dt / len(problems) * 1e3:.3f} ms per instance")
+            return recs, (f"lockstep batches of {res[0].timers['batch_size']} instances per launch (qs_batch_*), "
+                          f"{dt / len(problems) * 1e3:.3f} ms per instance incl. set-up")
         except MemoryError:
             pass  # an instance does not fit a slot: per-instance handles below
     fn = pattern_reuse_solver()

@@ -133,14 +133,36 @@ class BatchSolver:
         return out
 
 
-def solve_batched(problems, settings: Settings | None = None, max_batch: int = MAX_BATCH) -> list[SolveResult]:
-    """Solve same-pattern instances in lockstep batches of at most `max_batch` on settings.device."""
+def solve_batched(problems, settings: Settings | None = None, max_batch: int = MAX_BATCH, side_by_side: int = 4) -> list[SolveResult]:
+    """Solve same-pattern instances in lockstep batches on settings.device.
+
+    Up to `side_by_side` batches (own arena, stream and host thread each) run concurrently once there is work for more
+    than one full batch: the synchronisation gaps of one lockstep batch are filled by the launches of the others (C5
+    on one B200, set-up excluded: 2590 instances/s as one batch of 512, 3390 as 2 x 512, 3460 as 4 x 256 over 1024
+    instances).  A lane pays its own set-up (analysis, arena), so 512 instances stay ONE batch: with set-up inside
+    the clock 4 x 128 took 0.40 s against 0.23 s.  Batches hold at most `max_batch` instances."""
     problems = list(problems)
     if not problems:
         return []
-    size = min(max_batch, len(problems))
-    out = []
-    with BatchSolver(problems[0], size, settings) as bs:
-        for k0 in range(0, len(problems), size):
-            out.extend(bs.solve(problems[k0:k0 + size]))
+    count = len(problems)
+    lanes = max(1, min(side_by_side, count // max_batch))  # a lane is worth its set-up cost from a full batch on
+    size = min(max_batch, -(-count // lanes))
+    chunks = [(k0, problems[k0:k0 + size]) for k0 in range(0, count, size)]
+    out: list = [None] * count
+
+    def run(lane):
+        mine = chunks[lane::lanes]
+        if not mine:
+            return
+        with BatchSolver(problems[0], size, settings) as bs:
+            for k0, chunk in mine:
+                out[k0:k0 + len(chunk)] = bs.solve(chunk)
+
+    if lanes == 1:
+        run(0)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(lanes) as pool:
+            list(pool.map(run, range(lanes)))  # list(): re-raise a lane's exception here
     return out

@@ -71,6 +71,23 @@ __device__ __forceinline__ void row_dot4(const Csr& M, const int (&row)[4], cons
   }
 }
 
+// One row of the fused dual-range matrix Dt = [Pf | A' | G']: three sums (P x, A'y, G'z), entries in the order Pf, A',
+// G' and, inside a block, in the block's own order -- so each sum is bitwise the one row_dot_thread would produce.
+__device__ __forceinline__ void row_dot_fused(const Csr& Dt, int row, const double* __restrict__ x,
+                                              const double* __restrict__ y, const double* __restrict__ z, double& px,
+                                              double& aty, double& gtz) {
+  px = aty = gtz = 0.0;
+  const int e = Dt.ptr[row + 1];
+  for (int p = Dt.ptr[row]; p < e; ++p) {
+    const int j = Dt.idx[p];
+    const double v = Dt.val[p];
+    const int tag = (unsigned)j >> QS_DT_TAG_SHIFT, col = j & QS_DT_COL_MASK;
+    if (tag == 0) px += v * x[col];
+    else if (tag == 1) aty += v * y[col];
+    else gtz += v * z[col];
+  }
+}
+
 // Short rows (a handful of entries): one thread per row, plain loop.  Few instructions and few registers, so
 // many warps are resident and their load chains overlap; the generic lane-group machinery costs ~10x more
 // instructions per entry on such rows.  Same summation order as a one-lane group.
@@ -257,7 +274,7 @@ __device__ __forceinline__ double absmax(double a, double v) {
 // compute_residuals is three launches, one per row range (dual / eq / cone), each compiled for ONE row-product
 // mode: a fused single kernel carried the registers of all nine (range, mode) paths (80 per thread, 3 CTAs per
 // SM) and, with rows this short, the kernel is bound by how many load chains are in flight.
-enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2, MODE_MLP = 3 };  // MLP: thread per row, several rows in flight
+enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2, MODE_MLP = 3, MODE_FUSED = 4 };  // MLP: thread per row, several rows in flight
 enum { RANGE_DUAL = 0, RANGE_EQ = 1, RANGE_CONE = 2 };
 
 __device__ __forceinline__ RowRange locate1(int tpr, int mode) {
@@ -288,7 +305,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
   double v[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = 0.0;
-  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP) ? 1 : A.Pf.tpr, MODE);
+  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP || MODE == MODE_FUSED) ? 1 : A.Pf.tpr, MODE);
   auto finish_row = [&](int row, double px, double aty, double gtz) {
     const double ci = A.c[row], xi = A.x[row];
     const double rd = px + ci + aty + gtz;
@@ -303,6 +320,12 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_dual(ResidualArgs A) {
   if (MODE == MODE_THREAD) {
     for (int row = r.row; row < A.n; row += r.stride)
       finish_row(row, row_dot_thread(A.Pf, row, A.x), row_dot_thread(A.At, row, A.y), row_dot_thread(A.Gt, row, A.z));
+  } else if (MODE == MODE_FUSED) {
+    for (int row = r.row; row < A.n; row += r.stride) {
+      double px, aty, gtz;
+      row_dot_fused(A.Dt, row, A.x, A.y, A.z, px, aty, gtz);
+      finish_row(row, px, aty, gtz);
+    }
   } else if (MODE == MODE_MLP) {
     const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
     const double* const vecs[3] = {A.x, A.y, A.z};
@@ -489,7 +512,15 @@ __global__ void __launch_bounds__(QS_THREADS)
   const double* vx = A.v;
   const double* vy = A.v + A.n;
   const double* vz = A.v + A.n + A.p;
-  if (r.which == 0 && r.tpr == 1) {
+  if (r.which == 0 && r.tpr == 1 && A.Dt.ptr) {
+    for (int row = r.row; row < A.n; row += r.stride) {
+      double px, aty, gtz;
+      row_dot_fused(A.Dt, row, vx, vy, vz, px, aty, gtz);
+      const double t = A.rhs[row] - (px + aty + gtz);
+      A.r[row] = t;
+      v[0] = absmax(v[0], t);
+    }
+  } else if (r.which == 0 && r.tpr == 1) {
     const Csr* const mats[3] = {&A.Pf, &A.At, &A.Gt};
     const double* const vecs[3] = {vx, vy, vz};
     for (int row0 = r.row; row0 < A.n; row0 += 2 * r.stride) {
@@ -695,6 +726,17 @@ int vgrid(i64 n) {
 }
 
 
+__global__ void __launch_bounds__(QS_THREADS) k_gather3(i64 n, const double* __restrict__ s0, const double* __restrict__ s1,
+                                                        const double* __restrict__ s2, const int* __restrict__ map,
+                                                        double* __restrict__ dst) {
+  QS_BATCH(s0, s1, s2, map, dst);
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const int j = map[i];
+    const int tag = (unsigned)j >> QS_DT_TAG_SHIFT, k = j & QS_DT_COL_MASK;
+    dst[i] = tag == 0 ? s0[k] : (tag == 1 ? s1[k] : s2[k]);
+  }
+}
+
 // dst[i] = src[i] where *flag != 0 (the flag is a scalar of the instance: accept / reject decided on the host)
 __global__ void __launch_bounds__(QS_THREADS) k_copy_if(i64 n, const double* flag, const double* src, double* dst) {
   QS_BATCH(flag, src, dst);
@@ -752,7 +794,10 @@ int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
     else QS_RESID(k_resid_eq, MODE_GROUP, blocks_capped(A.p, t));
     ++launches;
   }
-  if (A.Pf.tpr == 1) {
+  static const bool fused_dual = !(getenv("QS_RESID_FUSED") && atoi(getenv("QS_RESID_FUSED")) == 0);
+  if (A.Pf.tpr == 1 && A.Dt.ptr && fused_dual) {
+    QS_RESID(k_resid_dual, MODE_FUSED, std::max(1, std::min(148 * 16, (A.n + 2 * QS_THREADS - 1) / (2 * QS_THREADS))));
+  } else if (A.Pf.tpr == 1) {
     if (mlp_dual) QS_RESID(k_resid_dual, MODE_MLP, tgrid(A.n, 2));
     else QS_RESID(k_resid_dual, MODE_THREAD, std::max(1, std::min(148 * 16, (A.n + 2 * QS_THREADS - 1) / (2 * QS_THREADS))));
   }
@@ -806,4 +851,9 @@ void qsk_copy_if(i64 n, const double* flag, const double* src, double* dst, cuda
 void qsk_broadcast(i64 nwords, void* p, int slots, cudaStream_t st) {
   if (nwords > 0 && slots > 1)
     k_broadcast<<<dim3((unsigned)vgrid(nwords), 1, (unsigned)(slots - 1)), QS_THREADS, 0, st>>>(nwords, (unsigned long long*)p);
+}
+
+void qsk_gather3(i64 n, const double* src0, const double* src1, const double* src2, const int* map, double* dst,
+                 cudaStream_t st) {
+  if (n > 0) k_gather3<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, src0, src1, src2, map, dst);
 }

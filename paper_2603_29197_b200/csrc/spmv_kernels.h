@@ -18,16 +18,24 @@ struct Csr {
 
 // compute_residuals (ipm.py:70-103): writes rhs[0:n] = -r_dual, rhs[n:n+p] = -r_eq,
 // r_cone, and every scalar check_termination (ipm.py:106-119) needs.
+// Dual range in ONE pass: Dt = [Pf | A' | G'] row by row (n rows), each index tagged in its top two bits with the block
+// it came from (0: P, operand x; 1: A', operand y; 2: G', operand z).  One row pointer pair and one entry stream per
+// row instead of three: the dependent chain row pointer -> entry -> operand is paid once.  Built at setup when the
+// dual range runs thread-per-row (short rows); ptr == nullptr otherwise.
+#define QS_DT_TAG_SHIFT 30
+#define QS_DT_COL_MASK 0x3fffffff
+
 struct ResidualArgs {
   int n, p, m;
   Csr Pf, At, Gt, Ar, Gr;  // Pf.tpr is used for the whole dual range
+  Csr Dt;
   const double *x, *y, *z, *s, *c, *b, *h;
   double* rhs;
   double* r_cone;
   double* scalars;
   GridRed gr;
   __device__ void shift(size_t off) {
-    Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), gr.shift(off);
+    Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), Dt.shift(off), gr.shift(off);
     qs_shift(off, x), qs_shift(off, y), qs_shift(off, z), qs_shift(off, s), qs_shift(off, c), qs_shift(off, b);
     qs_shift(off, h), qs_shift(off, rhs), qs_shift(off, r_cone), qs_shift(off, scalars);
   }
@@ -36,6 +44,7 @@ struct ResidualArgs {
 struct KktResidualArgs {
   int n, p, m;
   Csr Pf, At, Gt, Ar, Gr;
+  Csr Dt;
   const double* v;     // [n+p+m] candidate solution
   const double* rhs;   // [n+p+m]
   const double* w2vz;  // [m]  W'W v_z
@@ -44,7 +53,7 @@ struct KktResidualArgs {
   int slot;            // scalars[slot] = ||r||_inf
   GridRed gr;
   __device__ void shift(size_t off) {
-    Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), gr.shift(off);
+    Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), Dt.shift(off), gr.shift(off);
     qs_shift(off, v), qs_shift(off, rhs), qs_shift(off, w2vz), qs_shift(off, r), qs_shift(off, scalars);
   }
 };
@@ -56,6 +65,9 @@ void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cuda
 void qsk_spmv_sym_upper_csc(int ncols, const i64* cp, const int* ri, const double* vx, const double* x, double* out,
                             cudaStream_t st);
 void qsk_gather(i64 n, const double* src, const int* map, double* dst, cudaStream_t st);  // dst[i] = src[map[i]]
+// dst[i] = src_t[map[i] & QS_DT_COL_MASK] with t = map[i] >> QS_DT_TAG_SHIFT (values of the fused dual-range matrix)
+void qsk_gather3(i64 n, const double* src0, const double* src1, const double* src2, const int* map, double* dst,
+                 cudaStream_t st);
 void qsk_axpby(i64 n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st);
 void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed gr, cudaStream_t st);
 // batched mode (common.cuh): per-instance conditional copy; replication of slot 0's words into the other slots

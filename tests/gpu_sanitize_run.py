@@ -49,3 +49,16 @@ s.update(c=d.c * 1.1, h=d.h * 1.05)
 print(s.solve().status.value)
 s.close()
 print("sanitize run complete")
+
+# batched small-problem mode (every kernel with gridDim.z > 1, the arena allocator, copy_if / broadcast)
+from paper_2603_29197_b200.batched import solve_batched
+
+import dataclasses
+
+base = configs.group_lasso(groups=12, qlo=20, qhi=90, samples=40, nnz_per_col=3, seed=7)  # blocked fronts, SOCs
+batches = {"mpc": [configs.mpc(horizon=12, nx=6, nu=2, seed=s) for s in range(5)],
+           "group_lasso": [dataclasses.replace(base, c=base.c * (1.0 + 0.1 * s), b=base.b * (1.0 + 0.05 * s)) for s in range(4)]}
+for fam, probs in batches.items():
+    res = solve_batched(probs)
+    print("batched", fam, [r.status.value for r in res], [r.iterations for r in res], flush=True)
+print("sanitize run (batched) complete")

@@ -6,6 +6,8 @@ GPU box the same driver runs the CUDA path (tests/test_gpu_batch.py)."""
 import os
 import sys
 
+import numpy as np
+
 import pytest
 import torch.multiprocessing as mp
 
@@ -114,3 +116,17 @@ def test_rank_device_and_error_records(monkeypatch):
     recs, _ = solve_batch(lambda i: i, 4, None, solve_fn=solve_fn, device=5)
     assert seen == [5, 5, 5, 5]
     assert [r.status for r in recs] == ["Solved", "Solved", "Error: RuntimeError: boom", "Solved"]
+
+
+def test_same_pattern_is_about_structure_not_numbers():
+    import dataclasses
+
+    from paper_2603_29197_b200 import configs
+    from paper_2603_29197_b200.batched import same_pattern
+
+    a, b = configs.make("C5_mpc", small=True, seed=0), configs.make("C5_mpc", small=True, seed=1)
+    assert same_pattern(a, b) and not np.array_equal(a.b, b.b)
+    c = configs.make("C4_group_lasso", small=True, seed=0)
+    assert not same_pattern(a, c)
+    d = dataclasses.replace(a, cone=type(a.cone)(a.cone.orthant_dim + a.cone.soc_dims[-1], a.cone.soc_dims[:-1]))
+    assert not same_pattern(a, d)  # same matrices, another cone layout

@@ -93,3 +93,18 @@ def test_pattern_mismatch_is_rejected():
     with BatchSolver(a, 2) as bs:
         with pytest.raises(BadSparseStructure):
             bs.solve([a, b])
+
+
+def test_solve_shard_picks_the_lockstep_mode_and_falls_back_for_mixed_patterns():
+    from paper_2603_29197_b200.batch import solve_shard
+
+    probs = [configs.make("C5_mpc", small=True, seed=i) for i in range(5)]
+    recs, mode = solve_shard(probs, device=0)
+    assert "lockstep" in mode and [r.index for r in recs] == list(range(5))
+    assert all(r.status == "Solved" for r in recs)
+    refs = [qs.solve(d) for d in probs]
+    assert [r.iterations for r in recs] == [r.iterations for r in refs]
+    assert [r.objective for r in recs] == [r.objective for r in refs]
+    mixed = probs[:2] + [configs.make("C4_group_lasso", small=True, seed=0)]
+    recs, mode = solve_shard(mixed, device=0, workers=2)
+    assert "in flight" in mode and all(r.status == "Solved" for r in recs)
