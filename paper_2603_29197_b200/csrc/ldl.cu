@@ -1086,10 +1086,24 @@ __device__ void solve_fwd_body(const DevSym& S, int s, const double* L, double* 
   for (int e = tid; e < ns * ns; e += blockDim.x) L11[e] = f.Lp[(e % ns) + (i64)(e / ns) * nr];
   if (tid < ns) xs[tid] = x1[tid];
   __syncthreads();
-  for (int k = 0; k < ns - 1; ++k) {  // unit lower triangular solve at shared-memory latency
-    const double xk = xs[k];
-    for (int i = k + 1 + tid; i < ns; i += blockDim.x) xs[i] -= L11[i + k * ns] * xk;
+  if (ns <= 32) {
+    // one warp, entry i in lane i, pivots broadcast by shuffles: no CTA barrier per pivot (a chain of ~50 narrow
+    // levels per sweep pays every barrier in latency).  Same update order per entry as the loop below: bitwise equal.
+    if (tid < 32) {
+      double x = tid < ns ? xs[tid] : 0.0;
+      for (int k = 0; k < ns - 1; ++k) {
+        const double xk = __shfl_sync(0xffffffffu, x, k);
+        if (tid > k && tid < ns) x -= L11[tid + k * ns] * xk;
+      }
+      if (tid < ns) xs[tid] = x;
+    }
     __syncthreads();
+  } else {
+    for (int k = 0; k < ns - 1; ++k) {  // unit lower triangular solve at shared-memory latency
+      const double xk = xs[k];
+      for (int i = k + 1 + tid; i < ns; i += blockDim.x) xs[i] -= L11[i + k * ns] * xk;
+      __syncthreads();
+    }
   }
   if (tid < ns) x1[tid] = xs[tid];
   for (int r = tid; r < f.nu; r += blockDim.x) {
@@ -1129,10 +1143,22 @@ __device__ void solve_bwd_body(const DevSym& S, int s, const double* L, double* 
   }
   __syncthreads();
   // x1 <- L11^{-T} x1
-  for (int k = ns - 1; k > 0; --k) {
-    const double xk = xs[k];
-    for (int i = tid; i < k; i += blockDim.x) xs[i] -= L11[k + i * ns] * xk;
+  if (ns <= 32) {  // one warp, no CTA barrier per pivot (see solve_fwd_body); bitwise the loop below
+    if (tid < 32) {
+      double x = tid < ns ? xs[tid] : 0.0;
+      for (int k = ns - 1; k > 0; --k) {
+        const double xk = __shfl_sync(0xffffffffu, x, k);
+        if (tid < k) x -= L11[k + tid * ns] * xk;
+      }
+      if (tid < ns) xs[tid] = x;
+    }
     __syncthreads();
+  } else {
+    for (int k = ns - 1; k > 0; --k) {
+      const double xk = xs[k];
+      for (int i = tid; i < k; i += blockDim.x) xs[i] -= L11[k + i * ns] * xk;
+      __syncthreads();
+    }
   }
   if (tid < ns) x1[tid] = xs[tid];
 }

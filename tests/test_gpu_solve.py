@@ -271,3 +271,20 @@ def test_batch_with_pattern_reuse_matches_independent_solves():
     for ra, rb in zip(a, b):
         assert ra.index == rb.index and ra.status == rb.status == "Solved"
         assert ra.iterations == rb.iterations and ra.objective == rb.objective
+
+
+def test_linear_system_calls_replay_captured_graphs():
+    """On the handle's own (non-default) stream every factor / solve after the first of its kind is a CUDA-graph
+    replay (qs_get_graph_stats); QS_NO_GRAPH is the only path to direct launch sequences."""
+    from paper_2603_29197_b200.ipm import DeviceSolver
+
+    d = problem_from_golden(load_golden("portfolio_4"))
+    dev = DeviceSolver(d)
+    try:
+        status, iters, _ = dev.run()
+        st = dev.graph_stats()
+        f, s, _ = dev.counters()
+        assert status is SolveStatus.SOLVED
+        assert st["direct_launch_sequences"] == 0 and st["graph_replays"] >= f + s
+    finally:
+        dev.close()
