@@ -108,3 +108,20 @@ def test_solve_shard_picks_the_lockstep_mode_and_falls_back_for_mixed_patterns()
     mixed = probs[:2] + [configs.make("C4_group_lasso", small=True, seed=0)]
     recs, mode = solve_shard(mixed, device=0, workers=2)
     assert "in flight" in mode and all(r.status == "Solved" for r in recs)
+
+
+@pytest.mark.parametrize("family", ["C4_group_lasso", "C3_portfolio", "C2_lasso", "C1_random_qp"])
+def test_batch_of_other_families_exercises_every_front_path(family):
+    """Same pattern, different numbers, for the families whose factorisation uses leaf fronts, blocked fronts, DMMA
+    Schur updates and the clustered root solves: every batched launch path against the stand-alone solve, bitwise."""
+    import dataclasses
+
+    base = configs.make(family, small=True, seed=3)
+    rng = np.random.default_rng(5)
+    # the cost vector only: feasibility (b = A x0, h = G x0 + s0) stays as generated
+    probs = [base] + [dataclasses.replace(base, c=base.c * (1.0 + 0.2 * rng.random(base.c.size))) for _ in range(3)]
+    got = solve_batched(probs)
+    for d, r in zip(probs, got):
+        ref = qs.solve(d)
+        assert ref.status is SolveStatus.SOLVED, family
+        _same(r, ref)

@@ -9,8 +9,9 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,memory.total --format=csv > $OUT/gpu.txt 2>&1
 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $OUT/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $OUT/smoke.log
-python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
-python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
+# the two commands the driver runs at round end, with its flags
+T0=$SECONDS; python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$? wall $((SECONDS-T0)) s" | tee $OUT/bench_wall.txt
+T0=$SECONDS; python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "reference arm rc=$? wall $((SECONDS-T0)) s" | tee -a $OUT/bench_wall.txt
 python tests/gpu_microbench.py > $OUT/microbench.txt 2>&1
 # the other BASELINE configurations (parity-size cases, not the headline) and the C5 batch on one GPU
 for w in C1_random_qp C2_lasso C2_lasso_20k C3_portfolio C5_mpc; do
