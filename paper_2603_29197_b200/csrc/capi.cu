@@ -219,6 +219,7 @@ struct qs_handle {
   qs_settings st{};
   Csr Pf{}, At{}, Gt{}, Ar{}, Gr{}, Pu{};
   Csr Dt{};            // fused dual-range matrix [Pf | A' | G'] with tagged indices (spmv_kernels.h), or ptr == nullptr
+  double* seg_partial = nullptr;  // [p * QS_ROW_SEGS] when the equality rows are long (spmv_kernels.h)
   int* dt_map = nullptr;  // Dt.val[k] = {Pf, At, Gt}.val[dt_map[k] & mask] by tag
   i64 nnzDt = 0;
   // value maps for qs_update_values: Ar.val[k] = Ax[ar_map[k]], Gr.val[k] = Gx[gr_map[k]], Pf.val[k] = Px[pf_map[k]]
@@ -382,7 +383,7 @@ int solve_refined(qs_handle* h, const double* rhs) {
       h->launches += 3;
     } else {
       qsk_apply_w2(h->L, h->w, h->eta, h->wbar, v + h->n + h->p, h->w2vz, st);
-      KktResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt,
+      KktResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->seg_partial,
                         v,         rhs,       h->w2vz,   r,     h->scalars, slot, h->gr};
       qsk_kkt_residual(A, st);
       h->launches += 2;
@@ -1089,42 +1090,31 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   // one lane-group width for the whole dual range (three products per row)
   h->Pf.tpr = std::min(32, qsk_pick_tpr(std::max(std::max(nnzP * 2, nnzA), nnzG), n));  // no CTA-per-row mode here
   h->At.tpr = h->Gt.tpr = h->Pf.tpr;
+  if (h->Ar.tpr >= 256 && p > 0) {  // CTA-per-row class: the residual's equality range uses the split product
+    h->seg_partial = h->prob_pool.alloc<double>((size_t)p * QS_ROW_SEGS);
+    if (!h->seg_partial) return fail(h, QS_E_MEMORY, "out of device memory for the row-segment partials");
+  }
   if (h->Pf.tpr == 1 && n < (1 << QS_DT_TAG_SHIFT) && p < (1 << QS_DT_TAG_SHIFT) && m < (1 << QS_DT_TAG_SHIFT) &&
       Pfp[n] + nnzA + nnzG < ((i64)1 << 31) && std::max(std::max(Pfp[n], nnzA), nnzG) < (1 << QS_DT_TAG_SHIFT)) {
-    // short rows: the dual range reads ONE matrix [Pf | A' | G'] (tagged indices) instead of three
+    // short rows: the dual range reads ONE matrix [Pf | A' | G'] (tagged indices) instead of three; built on the
+    // device from the row views uploaded above
     const i64 nd = Pfp[n] + nnzA + nnzG;
-    std::vector<int> dp(n + 1), di(nd), dmap(nd);
-    std::vector<double> dv(nd);
-    i64 at = 0;
-    for (i64 r = 0; r < n; ++r) {
-      dp[r] = (int)at;
-      for (i64 k = Pfp[r]; k < Pfp[r + 1]; ++k, ++at) {
-        di[at] = (int)Pfi[k];
-        dmap[at] = (int)k;
-        dv[at] = Pfx[k];
-      }
-      for (i64 k = Ap[r]; k < Ap[r + 1]; ++k, ++at) {
-        di[at] = (int)Ai[k] | (1 << QS_DT_TAG_SHIFT);
-        dmap[at] = (int)k | (1 << QS_DT_TAG_SHIFT);
-        dv[at] = Ax[k];
-      }
-      for (i64 k = Gp[r]; k < Gp[r + 1]; ++k, ++at) {
-        di[at] = (int)((unsigned)Gi[k] | (2u << QS_DT_TAG_SHIFT));
-        dmap[at] = (int)((unsigned)k | (2u << QS_DT_TAG_SHIFT));
-        dv[at] = Gx[k];
-      }
-    }
-    dp[n] = (int)at;
+    int* dp = h->prob_pool.alloc<int>(n + 1);
+    int* di = h->prob_pool.alloc<int>(nd);
+    double* dv = h->prob_pool.alloc<double>(nd);
+    h->dt_map = h->prob_pool.alloc<int>(nd);
     h->Dt.rows = (int)n;
     h->Dt.cols = (int)(n + p + m);
-    h->Dt.ptr = h->prob_pool.upload(dp.data(), dp.size(), st);
-    h->Dt.idx = h->prob_pool.upload(di.data(), di.size(), st);
-    h->Dt.val = h->prob_pool.upload(dv.data(), dv.size(), st);
+    h->Dt.ptr = dp;
+    h->Dt.idx = di;
+    h->Dt.val = dv;
     h->Dt.tpr = 1;
     h->Dt.exact1 = 0;
-    h->dt_map = h->prob_pool.upload(dmap.data(), dmap.size(), st);
     h->nnzDt = nd;
-    cudaStreamSynchronize(st);  // the staging vectors die here
+    if (dp && di && dv && h->dt_map) {
+      qsk_build_dt((int)n, h->Pf, h->At, h->Gt, dp, di, dv, h->dt_map, st);
+      h->launches++;
+    }
     if (!h->Dt.ptr || !h->Dt.idx || !h->Dt.val || !h->dt_map) return fail(h, QS_E_MEMORY, "out of device memory for the fused dual-range matrix");
   }
   h->c = h->prob_pool.upload(c, n, st);
@@ -1432,7 +1422,7 @@ int qs_initialize_iterate(qs_handle* h, double* mu_host) {
 int qs_residuals(qs_handle* h, qs_residual_info* out) {
   NEED_PROBLEM(h)
   h->tm.begin(T_RESID, h->stream);
-  ResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->x, h->y, h->z, h->s,
+  ResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->seg_partial, h->x, h->y, h->z, h->s,
                  h->c,      h->b,      h->hv,     h->rhs, h->r_cone, h->scalars, h->gr};
   h->launches += qsk_residuals(A, h->stream);
   h->tm.end(h->stream);
@@ -1662,7 +1652,7 @@ static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, dou
       case 6: qsk_corrector_rhs(L, h->w, h->eta, h->wbar, h->lam, h->lam_sq, h->ds, h->wdz, h->r_cone, nullptr, h->tmp_m,
                                 h->w2vz, h->scalars, st); break;
       case 7: {
-        ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->x, h->y, h->z, h->s,
+        ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->seg_partial, h->x, h->y, h->z, h->s,
                        h->c,   h->b,   h->hv,  h->rhs, h->r_cone, h->scalars, h->gr};
         qsk_residuals(A, st);
         break;
@@ -1675,7 +1665,7 @@ static int time_kernel_impl(qs_handle* h, int kernel_id, int reps, int cold, dou
       case 13: h->ls.solve(h->rhs, h->dx, st); break;
       case 14: {
         qsk_apply_w2(L, h->w, h->eta, h->wbar, h->sol + n + p, h->w2vz, st);
-        KktResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt,
+        KktResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->seg_partial,
                           h->sol, h->rhs, h->w2vz, h->rb, h->scalars, SC_TMP3, h->gr};
         qsk_kkt_residual(A, st);
         break;
@@ -1808,7 +1798,7 @@ int solve_refined_b(qs_batch* bt, const double* rhs, std::vector<int>& status) {
   auto residual = [&](const double* v, double* rr, int slot) {
     h->tm.begin(T_REFINE, st);
     qsk_apply_w2(h->L, h->w, h->eta, h->wbar, v + h->n + h->p, h->w2vz, st);
-    KktResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt,
+    KktResidualArgs A{(int)h->n, (int)h->p, (int)h->m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->seg_partial,
                       v,         rhs,       h->w2vz,   rr,    h->scalars, slot, h->gr};
     qsk_kkt_residual(A, st);
     h->tm.end(st);
@@ -2079,7 +2069,7 @@ int qs_batch_solve(qs_batch* bt, int64_t* status_out, int64_t* iterations_out, d
   for (;;) {
     // compute_residuals (ipm.py:70-103) + check_termination (ipm.py:106-119)
     h->tm.begin(T_RESID, st);
-    ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->x, h->y, h->z, h->s,
+    ResidualArgs A{(int)n, (int)p, (int)m, h->Pf, h->At, h->Gt, h->Ar, h->Gr, h->Dt, h->seg_partial, h->x, h->y, h->z, h->s,
                    h->c,   h->b,   h->hv,  h->rhs, h->r_cone, h->scalars, h->gr};
     bt->launches += qsk_residuals(A, st);
     h->tm.end(st);

@@ -274,7 +274,7 @@ __device__ __forceinline__ double absmax(double a, double v) {
 // compute_residuals is three launches, one per row range (dual / eq / cone), each compiled for ONE row-product
 // mode: a fused single kernel carried the registers of all nine (range, mode) paths (80 per thread, 3 CTAs per
 // SM) and, with rows this short, the kernel is bound by how many load chains are in flight.
-enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2, MODE_MLP = 3, MODE_FUSED = 4 };  // MLP: thread per row, several rows in flight
+enum { MODE_THREAD = 0, MODE_GROUP = 1, MODE_CTA = 2, MODE_MLP = 3, MODE_FUSED = 4, MODE_SPLIT = 5 };  // MLP: thread per row, several rows in flight
 enum { RANGE_DUAL = 0, RANGE_EQ = 1, RANGE_CONE = 2 };
 
 __device__ __forceinline__ RowRange locate1(int tpr, int mode) {
@@ -293,6 +293,35 @@ __device__ __forceinline__ RowRange locate1(int tpr, int mode) {
   r.lane = threadIdx.x & (tpr - 1);
   r.mask = lane_mask(tpr);
   return r;
+}
+
+// partial[row * QS_ROW_SEGS + seg] = sum over segment `seg` of row `row` of M(row, :) x  -- a warp per segment
+template <bool BATCH>
+__global__ void __launch_bounds__(QS_THREADS) k_rowseg_partial(Csr M, const double* __restrict__ x, double* partial) {
+  if (BATCH) {
+    QS_BATCH(M, x, partial);
+  }
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= M.rows * QS_ROW_SEGS) return;
+  const int row = w / QS_ROW_SEGS, seg = w - row * QS_ROW_SEGS;
+  const int b = M.ptr[row];
+  const i64 len = M.ptr[row + 1] - b;
+  const int s0 = b + (int)(len * seg / QS_ROW_SEGS), s1 = b + (int)(len * (seg + 1) / QS_ROW_SEGS);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int p = s0 + lane;
+  for (; p + 96 < s1; p += 128) {
+    const int i0 = M.idx[p], i1 = M.idx[p + 32], i2 = M.idx[p + 64], i3 = M.idx[p + 96];
+    const double v0 = M.val[p], v1 = M.val[p + 32], v2 = M.val[p + 64], v3 = M.val[p + 96];
+    a0 += v0 * x[i0];
+    a1 += v1 * x[i1];
+    a2 += v2 * x[i2];
+    a3 += v3 * x[i3];
+  }
+  for (; p < s1; p += 32) a0 += M.val[p] * x[M.idx[p]];
+  double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) partial[w] = acc;
 }
 
 // r_dual = P x + c + A'y + G'z (ipm.py:76), -r_dual -> rhs[0:n]; |Px|, |A'y|, |G'z|, |r_dual| (inf norms), x'Px, c'x
@@ -375,7 +404,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
   }
   enum { AX, RE, NV };
   double v[NV] = {0.0, 0.0};
-  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP) ? 1 : A.Ar.tpr, MODE);
+  const RowRange r = locate1((MODE == MODE_THREAD || MODE == MODE_MLP || MODE == MODE_SPLIT) ? 1 : A.Ar.tpr, MODE);
   auto finish_row = [&](int row, double ax) {
     const double re = ax - A.b[row];
     A.rhs[A.n + row] = -re;
@@ -384,6 +413,13 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_eq(ResidualArgs A) {
   };
   if (MODE == MODE_THREAD) {
     for (int row = r.row; row < A.p; row += r.stride) finish_row(row, row_dot_thread(A.Ar, row, A.x));
+  } else if (MODE == MODE_SPLIT) {  // the products were formed by k_rowseg_partial: add the segments in order
+    for (int row = r.row; row < A.p; row += r.stride) {
+      double ax = 0.0;
+#pragma unroll
+      for (int sg = 0; sg < QS_ROW_SEGS; ++sg) ax += A.seg_partial[row * QS_ROW_SEGS + sg];
+      finish_row(row, ax);
+    }
   } else if (MODE == MODE_MLP) {
     const Csr* const mats[1] = {&A.Ar};
     const double* const vecs[1] = {A.x};
@@ -505,10 +541,10 @@ __global__ void __launch_bounds__(QS_THREADS) k_resid_cone(ResidualArgs A) {
 // plus ||r||_inf -> scalars[slot].  Reference: ldl.py:152,159 (there the
 // product runs over the stored entries of K; same operator, other rounding).
 __global__ void __launch_bounds__(QS_THREADS)
-    k_kkt_residual(KktResidualArgs A, int nbd, int nbe, int nbc) {
+    k_kkt_residual(KktResidualArgs A, int nbd, int nbe, int nbc, int eq_split) {
   QS_BATCH(A);
   double v[1] = {0.0};
-  const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, A.Ar.tpr, A.Gr.tpr);
+  const RowRange r = locate(nbd, nbe, nbc, A.Pf.tpr, eq_split ? 1 : A.Ar.tpr, A.Gr.tpr);
   const double* vx = A.v;
   const double* vy = A.v + A.n;
   const double* vz = A.v + A.n + A.p;
@@ -551,6 +587,15 @@ __global__ void __launch_bounds__(QS_THREADS)
           v[0] = absmax(v[0], t);
         }
       }
+    }
+  } else if (r.which == 1 && eq_split) {  // products formed by k_rowseg_partial: add the segments in order
+    for (int row = r.row; row < A.p; row += r.stride) {
+      double ax = 0.0;
+#pragma unroll
+      for (int sg = 0; sg < QS_ROW_SEGS; ++sg) ax += A.seg_partial[row * QS_ROW_SEGS + sg];
+      const double t = A.rhs[A.n + row] - ax;
+      A.r[A.n + row] = t;
+      v[0] = absmax(v[0], t);
     }
   } else if (r.which == 1 && r.tpr == QS_TPR_CTA) {
     __shared__ double rsm[QS_THREADS / 32];
@@ -737,6 +782,34 @@ __global__ void __launch_bounds__(QS_THREADS) k_gather3(i64 n, const double* __r
   }
 }
 
+// Dt = [Pf | At | Gt] row by row with tagged indices (spmv_kernels.h), built on the device from the three row views
+// that are already there: a thread per row (the host version of this loop cost 0.08 s at C4, more than the fused
+// matrix saves in a whole solve).
+__global__ void __launch_bounds__(QS_THREADS) k_build_dt(int n, Csr Pf, Csr At, Csr Gt, int* dp, int* di, double* dv,
+                                                         int* dmap) {
+  QS_BATCH(Pf, At, Gt, dp, di, dv, dmap);
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row > n) return;
+  int at = Pf.ptr[row] + At.ptr[row] + Gt.ptr[row];
+  dp[row] = at;
+  if (row == n) return;
+  for (int k = Pf.ptr[row]; k < Pf.ptr[row + 1]; ++k, ++at) {
+    di[at] = Pf.idx[k];
+    dmap[at] = k;
+    dv[at] = Pf.val[k];
+  }
+  for (int k = At.ptr[row]; k < At.ptr[row + 1]; ++k, ++at) {
+    di[at] = At.idx[k] | (1 << QS_DT_TAG_SHIFT);
+    dmap[at] = k | (1 << QS_DT_TAG_SHIFT);
+    dv[at] = At.val[k];
+  }
+  for (int k = Gt.ptr[row]; k < Gt.ptr[row + 1]; ++k, ++at) {
+    di[at] = (int)((unsigned)Gt.idx[k] | (2u << QS_DT_TAG_SHIFT));
+    dmap[at] = (int)((unsigned)k | (2u << QS_DT_TAG_SHIFT));
+    dv[at] = Gt.val[k];
+  }
+}
+
 // dst[i] = src[i] where *flag != 0 (the flag is a scalar of the instance: accept / reject decided on the host)
 __global__ void __launch_bounds__(QS_THREADS) k_copy_if(i64 n, const double* flag, const double* src, double* dst) {
   QS_BATCH(flag, src, dst);
@@ -771,6 +844,7 @@ int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
   static const int mlp_env = getenv("QS_RESID_MLP") ? atoi(getenv("QS_RESID_MLP")) : 1;
   static const bool mlp = mlp_env != 0;
   static const bool mlp_dual = mlp_env == 2;
+  static const bool split_rows = !(getenv("QS_RESID_SPLIT") && atoi(getenv("QS_RESID_SPLIT")) == 0);
   auto tgrid = [](int rows, int per) {
     if (!mlp) return std::max(1, std::min(148 * 16, (rows + 2 * QS_THREADS - 1) / (2 * QS_THREADS)));
     return std::max(1, std::min(148 * 8, (rows + per * QS_THREADS - 1) / (per * QS_THREADS)));
@@ -790,7 +864,13 @@ int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
   if (A.p > 0) {  // rows of A are the long ones when A is a design matrix: start them first
     const int t = A.Ar.tpr;
     if (t == 1) QS_RESID_T(k_resid_eq, A.p, 4);
-    else if (t == QS_TPR_CTA) QS_RESID(k_resid_eq, MODE_CTA, blocks_for(A.p, t));
+    else if (t == QS_TPR_CTA && A.seg_partial && split_rows) {
+      const int nw = A.p * QS_ROW_SEGS, nb = (nw * 32 + QS_THREADS - 1) / QS_THREADS;
+      if (bt) k_rowseg_partial<true><<<qs_grid(nb), QS_THREADS, 0, st>>>(A.Ar, A.x, A.seg_partial);
+      else k_rowseg_partial<false><<<qs_grid(nb), QS_THREADS, 0, st>>>(A.Ar, A.x, A.seg_partial);
+      QS_RESID(k_resid_eq, MODE_SPLIT, (A.p + QS_THREADS - 1) / QS_THREADS);
+      ++launches;
+    } else if (t == QS_TPR_CTA) QS_RESID(k_resid_eq, MODE_CTA, blocks_for(A.p, t));
     else QS_RESID(k_resid_eq, MODE_GROUP, blocks_capped(A.p, t));
     ++launches;
   }
@@ -814,8 +894,16 @@ int qsk_residuals(const ResidualArgs& A, cudaStream_t st) {
 }
 
 void qsk_kkt_residual(const KktResidualArgs& A, cudaStream_t st) {
-  const int nbd = blocks_capped(A.n, A.Pf.tpr, 2), nbe = blocks_capped(A.p, A.Ar.tpr), nbc = blocks_capped(A.m, A.Gr.tpr);
-  k_kkt_residual<<<qs_grid(nbd + nbe + nbc), QS_THREADS, 0, st>>>(A, nbd, nbe, nbc);
+  static const bool split_rows = !(getenv("QS_RESID_SPLIT") && atoi(getenv("QS_RESID_SPLIT")) == 0);
+  const int eq_split = A.p > 0 && A.Ar.tpr == QS_TPR_CTA && A.seg_partial && split_rows;
+  if (eq_split) {
+    const int nw = A.p * QS_ROW_SEGS, nb = (nw * 32 + QS_THREADS - 1) / QS_THREADS;
+    if (qs_tls_batch > 1) k_rowseg_partial<true><<<qs_grid(nb), QS_THREADS, 0, st>>>(A.Ar, A.v, A.seg_partial);
+    else k_rowseg_partial<false><<<qs_grid(nb), QS_THREADS, 0, st>>>(A.Ar, A.v, A.seg_partial);
+  }
+  const int nbd = blocks_capped(A.n, A.Pf.tpr, 2), nbc = blocks_capped(A.m, A.Gr.tpr);
+  const int nbe = eq_split ? (A.p + QS_THREADS - 1) / QS_THREADS : blocks_capped(A.p, A.Ar.tpr);
+  k_kkt_residual<<<qs_grid(nbd + nbe + nbc), QS_THREADS, 0, st>>>(A, nbd, nbe, nbc, eq_split);
 }
 
 void qsk_spmv_csr(const Csr& M, const double* x, double* y, int accumulate, cudaStream_t st) {
@@ -856,4 +944,9 @@ void qsk_broadcast(i64 nwords, void* p, int slots, cudaStream_t st) {
 void qsk_gather3(i64 n, const double* src0, const double* src1, const double* src2, const int* map, double* dst,
                  cudaStream_t st) {
   if (n > 0) k_gather3<<<qs_grid(vgrid(n)), QS_THREADS, 0, st>>>(n, src0, src1, src2, map, dst);
+}
+
+void qsk_build_dt(int n, const Csr& Pf, const Csr& At, const Csr& Gt, int* dp, int* di, double* dv, int* dmap,
+                  cudaStream_t st) {
+  k_build_dt<<<qs_grid((n + 1 + QS_THREADS - 1) / QS_THREADS), QS_THREADS, 0, st>>>(n, Pf, At, Gt, dp, di, dv, dmap);
 }

@@ -22,6 +22,10 @@ struct Csr {
 // it came from (0: P, operand x; 1: A', operand y; 2: G', operand z).  One row pointer pair and one entry stream per
 // row instead of three: the dependent chain row pointer -> entry -> operand is paid once.  Built at setup when the
 // dual range runs thread-per-row (short rows); ptr == nullptr otherwise.
+// Long rows (mean >= 512 entries: the sample rows of a design matrix) are cut into QS_ROW_SEGS segments, a warp per
+// segment with eight loads in flight per lane and no barrier; a second, tiny pass adds the partials of a row in
+// fixed order.  (A CTA per row spent a third of its stall cycles at its two barriers: ncu r02e.)
+#define QS_ROW_SEGS 8
 #define QS_DT_TAG_SHIFT 30
 #define QS_DT_COL_MASK 0x3fffffff
 
@@ -29,6 +33,7 @@ struct ResidualArgs {
   int n, p, m;
   Csr Pf, At, Gt, Ar, Gr;  // Pf.tpr is used for the whole dual range
   Csr Dt;
+  double* seg_partial;  // [p * QS_ROW_SEGS] scratch of the split long-row product of the equality range, or null
   const double *x, *y, *z, *s, *c, *b, *h;
   double* rhs;
   double* r_cone;
@@ -37,7 +42,7 @@ struct ResidualArgs {
   __device__ void shift(size_t off) {
     Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), Dt.shift(off), gr.shift(off);
     qs_shift(off, x), qs_shift(off, y), qs_shift(off, z), qs_shift(off, s), qs_shift(off, c), qs_shift(off, b);
-    qs_shift(off, h), qs_shift(off, rhs), qs_shift(off, r_cone), qs_shift(off, scalars);
+    qs_shift(off, h), qs_shift(off, rhs), qs_shift(off, r_cone), qs_shift(off, scalars), qs_shift(off, seg_partial);
   }
 };
 
@@ -45,6 +50,7 @@ struct KktResidualArgs {
   int n, p, m;
   Csr Pf, At, Gt, Ar, Gr;
   Csr Dt;
+  double* seg_partial;  // as in ResidualArgs, or null
   const double* v;     // [n+p+m] candidate solution
   const double* rhs;   // [n+p+m]
   const double* w2vz;  // [m]  W'W v_z
@@ -55,6 +61,7 @@ struct KktResidualArgs {
   __device__ void shift(size_t off) {
     Pf.shift(off), At.shift(off), Gt.shift(off), Ar.shift(off), Gr.shift(off), Dt.shift(off), gr.shift(off);
     qs_shift(off, v), qs_shift(off, rhs), qs_shift(off, w2vz), qs_shift(off, r), qs_shift(off, scalars);
+    qs_shift(off, seg_partial);
   }
 };
 
@@ -73,3 +80,6 @@ void qsk_absmax(i64 n, const double* x, double* out, double* nonfinite, GridRed 
 // batched mode (common.cuh): per-instance conditional copy; replication of slot 0's words into the other slots
 void qsk_copy_if(i64 n, const double* flag, const double* src, double* dst, cudaStream_t st);
 void qsk_broadcast(i64 nwords, void* p, int slots, cudaStream_t st);
+// Dt = [Pf | At | Gt] with tagged indices, plus the value map for qsk_gather3 (all arrays preallocated)
+void qsk_build_dt(int n, const Csr& Pf, const Csr& At, const Csr& Gt, int* dp, int* di, double* dv, int* dmap,
+                  cudaStream_t st);
