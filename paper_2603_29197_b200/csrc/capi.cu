@@ -1453,7 +1453,13 @@ int qs_step(qs_handle* h, qs_step_info* out) {
   rc = do_factor(h);
   if (rc) return rc;
   rc = solve_refined(h, h->rhs);
-  if (rc) return rc;
+  if (rc) {
+    // a point outside the cone poisons the scaling and with it the solve: report what the reference would have
+    // raised first (compute_nt_scaling -> NotInterior, cones.py:169-170,182-183); the scalars were fetched by the solve
+    if (rc == QS_E_NUMERICAL && h->scalars_host[SC_FLAG_NOT_INTERIOR] != 0.0)
+      return fail(h, QS_E_NOT_INTERIOR, "point is not strictly inside the cone");
+    return rc;
+  }
   h->tm.begin(T_CONE, st);
   // predictor: ds_a, W dz_a, both steps, alpha_aff, mu_aff, sigma
   qsk_post_solve(L, h->w, h->eta, h->wbar, h->d, h->sol + n + p, h->s, h->z, h->wdz, h->ds, h->scalars, 0,
@@ -1821,8 +1827,8 @@ int solve_refined_b(qs_batch* bt, const double* rhs, std::vector<int>& status) {
     stop[b] = 1e-12 * (1.0 + sc[SC_TMP0]);  // ldl.py:19,151
     rn[b] = sc[SC_TMP1];
     if (status[b] != BS_RUNNING) continue;
-    if (!(fabs(rn[b]) <= DBL_MAX)) {
-      status[b] = BS_NUMERICAL;  // non-finite triangular solve result
+    if (!(fabs(rn[b]) <= DBL_MAX)) {  // non-finite triangular solve result (a point outside the cone poisons it)
+      status[b] = sc[SC_FLAG_NOT_INTERIOR] != 0.0 ? BS_NOT_INTERIOR : BS_NUMERICAL;
       continue;
     }
     active[b] = rn[b] > stop[b];

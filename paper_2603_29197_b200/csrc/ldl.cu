@@ -1286,6 +1286,17 @@ void launch_clustered(void (*kern)(Args...), int nfronts, int cl, cudaStream_t s
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Threads of the single-CTA chain kernels (runs of narrow levels: a handful of small fronts per level).  Their
+// bodies are written for any block size; with fronts of ~30 rows most of 256 threads only wait at the barriers.
+int chain_threads() {
+  static const int t = [] {
+    int v = getenv("QS_CHAIN_THREADS") ? atoi(getenv("QS_CHAIN_THREADS")) : LDL_THREADS;
+    v = (v / 32) * 32;
+    return v < 32 ? 32 : (v > LDL_THREADS ? LDL_THREADS : v);
+  }();
+  return t;
+}
+
 int grid_for(i64 n) {
   i64 g = (n + LDL_THREADS - 1) / LDL_THREADS;
   if (g < 1) g = 1;
@@ -1730,7 +1741,7 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
   for (int lv = 0; lv < S.nlevels; ++lv) {
     if (chain_end[lv] > lv + 1) {  // a run of narrow levels: one single-CTA launch
       const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
-      k_chain_factor<<<qs_grid(1), LDL_THREADS, 0, st>>>(D, A, C, L, U, Dg, reg, dyn_eps, scalars);
+      k_chain_factor<<<qs_grid(1), chain_threads(), 0, st>>>(D, A, C, L, U, Dg, reg, dyn_eps, scalars);
       lv = chain_end[lv] - 1;
       continue;
     }
@@ -1826,7 +1837,7 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
   for (int lv = 0; lv < S.nlevels; ++lv) {
     if (chain_end[lv] > lv + 1) {
       const ChainArgs C{lv, chain_end[lv], d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
-      k_chain_fwd<<<qs_grid(1), LDL_THREADS, 0, st>>>(D, A, C, L, xw, B);
+      k_chain_fwd<<<qs_grid(1), chain_threads(), 0, st>>>(D, A, C, L, xw, B);
       lv = chain_end[lv] - 1;
       continue;
     }
@@ -1869,7 +1880,7 @@ void LinSys::solve_launches(const double* d_rhs, double* d_sol, cudaStream_t st)
     if (chain_start_of_end[lv] >= 0) {
       const int b = chain_start_of_end[lv];
       const ChainArgs C{b, lv + 1, d_smallptr, d_small, d_eaptr, d_eaitems, d_lvslot};
-      k_chain_bwd<<<qs_grid(1), LDL_THREADS, 0, st>>>(D, C, L, xw);
+      k_chain_bwd<<<qs_grid(1), chain_threads(), 0, st>>>(D, C, L, xw);
       lv = b;
       continue;
     }

@@ -288,3 +288,45 @@ def test_linear_system_calls_replay_captured_graphs():
         assert st["direct_launch_sequences"] == 0 and st["graph_replays"] >= f + s
     finally:
         dev.close()
+
+
+def test_a_failed_step_leaves_the_last_good_iterate():
+    """The reference builds the next iterate and raises BEFORE it replaces the current one (ipm.py:219-235), so a
+    NumericalError / NotInterior result carries the last good iterate.  Here the step writes to shadow buffers that are
+    swapped in only when no flag was raised."""
+    from paper_2603_29197_b200.errors import NotInterior, NumericalError
+
+    d = problem_from_golden(load_golden("portfolio_4"))
+    dev = DeviceSolver(d)
+    try:
+        dev.initialize_iterate()
+        dev.compute_residuals()
+        dev.ipm_step()
+        good = dev.iterate()
+        # (1) a point outside the cone: the step raises NotInterior and must not touch the iterate
+        s_bad = good.s.copy()
+        s_bad[0] = -1.0
+        dev.set_iterate(s=s_bad)
+        with pytest.raises(NotInterior):
+            dev.ipm_step()
+        after = dev.iterate()
+        assert np.array_equal(after.x, good.x) and np.array_equal(after.z, good.z) and np.array_equal(after.s, s_bad)
+        # (2) a non-finite direction (NaN right-hand side through y): NumericalError, iterate untouched
+        dev.set_iterate(s=good.s)
+        y_bad = good.y.copy()
+        y_bad[0] = np.nan
+        dev.set_iterate(y=y_bad)
+        with pytest.raises(NumericalError):
+            dev.compute_residuals()
+        with pytest.raises(NumericalError):
+            dev.ipm_step()
+        after = dev.iterate()
+        assert np.array_equal(after.x, good.x) and np.array_equal(after.z, good.z) and np.array_equal(after.s, good.s)
+        # and the driver reports NUMERICAL_ERROR for such data instead of raising (ipm.py:292-293)
+        bad = problem_from_golden(load_golden("portfolio_4"))
+        bad.b = bad.b.copy()
+        bad.b[0] = np.inf
+        res = qs.solve(bad)
+        assert res.status is SolveStatus.NUMERICAL_ERROR
+    finally:
+        dev.close()
