@@ -1037,7 +1037,7 @@ std::string hs_symbolic_cliques(i64 N, const i64* Kp, const i64* Ki, int order, 
     const i64 ns = S->col0[s + 1] - S->col0[s], nr = S->rowptr[s + 1] - S->rowptr[s], nu = nr - ns;
     S->relptr[s + 1] = S->relptr[s] + nu;
     S->Loff[s + 1] = S->Loff[s] + nr * ns;
-    S->Uoff[s + 1] = S->Uoff[s] + nu * nu;
+    S->Uoff[s + 1] = S->Uoff[s] + nu * (nu + 1) / 2;  // packed lower triangle (ldl.cu: qs_ucol)
     S->Boff[s + 1] = S->Boff[s] + nu;
     S->lnz += ns * (ns + 1) / 2 + nu * ns;
     for (i64 k = 0; k < ns; ++k) {

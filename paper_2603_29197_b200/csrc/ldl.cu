@@ -22,6 +22,11 @@ struct Front {
   double* Up;
 };
 
+// Update matrices are symmetric: only the lower triangle is stored, packed by columns (column j holds rows j..nu-1),
+// nu (nu + 1) / 2 doubles per front -- half the memory and half the zero-fill of a full nu x nu square (C4: 13 -> 6.5 GB;
+// SURVEY's denser C4, 170 GB of squares, fits only in this form).  Element (i, j), i >= j, is Up[qs_ucol(j, nu) + i].
+__device__ __forceinline__ i64 qs_ucol(i64 j, i64 nu) { return j * nu - j * (j + 1) / 2; }
+
 __device__ __forceinline__ Front front_of(const DevSym& S, int s, double* L, double* U) {
   Front f;
   f.c0 = S.col0[s];
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const int pc = it.c_lo + warp;
   if (pc >= f.nr) return;
   const i64 nr = f.nr, nu = f.nu;
-  double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;  // indexed by parent row
+  double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + qs_ucol(pc - f.ns, nu) - f.ns;  // indexed by parent row
   const int ch0 = S.childptr[s], ch1 = S.childptr[s + 1];
   for (int base = ch0; base < ch1; base += 32) {
     int hit = -1;
@@ -129,7 +134,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
       const int c = S.child[base + src];
       const int nsc = S.col0[c + 1] - S.col0[c];
       const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - nsc;
-      const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+      const double* Ucol = U + S.Uoff[c] + qs_ucol(cc, nuc);
       const int* rel = S.rel + S.relptr[c];
       for (int r = cc + lane; r < nuc; r += 32) dstcol[rel[r]] += Ucol[r];
     }
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
   const int s = A.slot_front[it.slot], pc = A.slot_row[it.slot];
   const Front f = front_of(S, s, L, U);
   const i64 nr = f.nr, nu = f.nu;
-  double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;  // indexed by parent row
+  double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + qs_ucol(pc - f.ns, nu) - f.ns;  // indexed by parent row
   const i64 e0 = on ? A.gptr[it.slot] : 0, e1 = on ? A.gptr[it.slot + 1] : 0;
   if (TPR == 32) {
     for (i64 eb = e0; eb < e1; eb += 32) {
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
           r_lo = max(cc, bs[it.band]);
           r_hi = bs[it.band + 1];
         }
-        uoff = S.Uoff[c] + (i64)cc * nuc;
+        uoff = S.Uoff[c] + qs_ucol(cc, nuc);
         roff = S.relptr[c];
       }
       const int cnt = (int)min((i64)32, e1 - eb);
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
         r_lo = max(cc, bs[it.band]);
         r_hi = bs[it.band + 1];
       }
-      const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+      const double* Ucol = U + S.Uoff[c] + qs_ucol(cc, nuc);
       const int* rel = S.rel + S.relptr[c];
       for (int r = r_lo + lane; r < r_hi; r += TPR) dstcol[rel[r]] += Ucol[r];
     }
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(LDL_THREADS)
   if (lane < nu) Lp[1 + lane] = l;
   for (int j = 0; j < nu; ++j) {
     const double lj = __shfl_sync(mask, l, j, G);
-    if (lane >= j && lane < nu) Up[lane + (i64)j * nu] -= a * lj;
+    if (lane >= j && lane < nu) Up[qs_ucol(j, nu) + lane] -= a * lj;
   }
 }
 
@@ -352,7 +357,7 @@ __device__ void front_factor_body(const DevSym& S, int s, double* L, double* U, 
           const double t = L21[j + k * nr] * dsm[k];
           if (i < nu) acc += L21[i + k * nr] * t;
         }
-        if (i < nu) f.Up[i + (i64)j * nu] -= acc;
+        if (i < nu) f.Up[qs_ucol(j, nu) + i] -= acc;
       }
     }
   }
@@ -608,7 +613,7 @@ __global__ void __launch_bounds__(LDL_THREADS, 3)
         const int gi = i0 + wi + 8 * a + g;
         if (gi >= f.nr || gi < gj) continue;
         if (SCHUR)
-          f.Up[(gi - f.ns) + (i64)(gj - f.ns) * f.nu] -= acc[a][b2][h];
+          f.Up[qs_ucol(gj - f.ns, f.nu) + (gi - f.ns)] -= acc[a][b2][h];
         else
           f.Lp[gi + (i64)gj * nr] -= acc[a][b2][h];
       }
@@ -1200,12 +1205,12 @@ __global__ void __launch_bounds__(LDL_THREADS)
       const int s = A.slot_front[it.slot], pc = A.slot_row[it.slot];
       const Front f = front_of(S, s, L, U);
       const i64 nr = f.nr, nu = f.nu;
-      double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + (i64)(pc - f.ns) * nu - f.ns;
+      double* dstcol = (pc < f.ns) ? f.Lp + pc * nr : f.Up + qs_ucol(pc - f.ns, nu) - f.ns;
       for (i64 e = A.gptr[it.slot]; e < A.gptr[it.slot + 1]; ++e) {
         const int c = A.gchild[e];
         const int cc = A.gsrc[e] - (int)S.Boff[c];
         const int nuc = (int)(S.rowptr[c + 1] - S.rowptr[c]) - (S.col0[c + 1] - S.col0[c]);
-        const double* Ucol = U + S.Uoff[c] + (i64)cc * nuc;
+        const double* Ucol = U + S.Uoff[c] + qs_ucol(cc, nuc);
         const int* rel = S.rel + S.relptr[c];
         for (int r = cc + lane; r < nuc; r += 32) dstcol[rel[r]] += Ucol[r];
       }

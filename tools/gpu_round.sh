@@ -14,7 +14,7 @@ T0=$SECONDS; python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.json 2>
 T0=$SECONDS; python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "reference arm rc=$? wall $((SECONDS-T0)) s" | tee -a $OUT/bench_wall.txt
 python tests/gpu_microbench.py > $OUT/microbench.txt 2>&1
 # the other BASELINE configurations (parity-size cases, not the headline) and the C5 batch on one GPU
-for w in C1_random_qp C2_lasso C2_lasso_20k C3_portfolio C5_mpc; do
+for w in C1_random_qp C2_lasso C2_lasso_20k C3_portfolio C5_mpc C4_group_lasso_survey; do
   python bench.py --workload $w --no-batch --cpu-budget 20 > $OUT/bench_$w.json 2> $OUT/bench_$w.err
 done
 python tests/gpu_batched_throughput.py 512 > $OUT/c5_batched_throughput.txt 2>&1

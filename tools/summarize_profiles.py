@@ -28,7 +28,7 @@ os.makedirs(dst, exist_ok=True)
 
 for name in ("bench.json", "bench_reference.json", "microbench.txt", "pytest_gpu.log", "smoke.log", "gpu.txt",
              "bench_torchrun1.json", "bench_C1_random_qp.json", "bench_C2_lasso.json", "bench_C3_portfolio.json",
-             "bench_C5_mpc.json", "bench_C2_lasso_20k.json", "c5_batch_throughput.txt", "c5_batched_throughput.txt",
+             "bench_C5_mpc.json", "bench_C2_lasso_20k.json", "bench_C4_group_lasso_survey.json", "c5_batch_throughput.txt", "c5_batched_throughput.txt",
              "ldl_factor_solve_ms.txt"):
     p = os.path.join(src, name)
     if os.path.exists(p) and os.path.getsize(p) > 0:
