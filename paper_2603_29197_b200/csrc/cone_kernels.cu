@@ -740,6 +740,7 @@ struct CorrRhsOp {
 // the kernel therefore accumulates the four dots s.z, s.dz, ds.z, ds.dz (its operands are in registers anyway)
 // and the last block evaluates s.z + alpha (s.dz + ds.z) + alpha^2 ds.dz -- the same polynomial the reference
 // sums term by term, rounded differently (relative difference of mu_aff ~1e-15 mu / mu_aff).
+template <bool CORR>
 struct PostSolveOp {
   static constexpr bool kResident = true;
   const double* w;
@@ -752,7 +753,7 @@ struct PostSolveOp {
   double* wdz;  // may be null (corrector does not need it)
   double* ds;
   double* scalars;
-  int corrector;
+  static constexpr int corrector = CORR;  // compile-time: the corrector instantiation carries no mu_aff sums
   double step_fraction;
   double deg;
   GridRed gr;
@@ -1152,7 +1153,8 @@ void qsk_post_solve(const ConeLayout& L, const double* w, const double* eta, con
                     const double* dz, const double* s, const double* z, double* wdz, double* ds, double* scalars,
                     int corrector, double step_fraction, double deg, GridRed gr, cudaStream_t st) {
   if (QS_EMPTY_GUARD(L)) return;
-  launch(L, PostSolveOp{w, eta, wbar, d, dz, s, z, wdz, ds, scalars, corrector, step_fraction, deg, gr}, st);
+  if (corrector) launch(L, PostSolveOp<true>{w, eta, wbar, d, dz, s, z, wdz, ds, scalars, step_fraction, deg, gr}, st);
+  else launch(L, PostSolveOp<false>{w, eta, wbar, d, dz, s, z, wdz, ds, scalars, step_fraction, deg, gr}, st);
 }
 
 void qsk_update_iterate(int n, int p, int m, const double* x, const double* y, const double* z, const double* s,
