@@ -301,7 +301,7 @@ def batch_throughput(rank, world, device, count=BATCH_COUNT, workers=8):
 
     mine = shard(count, rank, world)
     probs = {i: configs.make("C5_mpc", seed=i) for i in mine}
-    solve_shard([probs[mine[0]]] * min(len(mine), workers), device, workers)  # warm-up
+    solve_shard([probs[i] for i in mine], device, workers)  # warm-up: one untimed pass of the same shape
     t = time.perf_counter()
     recs, mode = solve_shard([probs[i] for i in mine], device, workers)
     return time.perf_counter() - t, recs, mode

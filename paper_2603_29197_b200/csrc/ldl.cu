@@ -183,12 +183,38 @@ __global__ void __launch_bounds__(LDL_THREADS)
         roff = S.relptr[c];
       }
       const int cnt = (int)min((i64)32, e1 - eb);
-      for (int q = 0; q < cnt; ++q) {  // fixed child order
-        const i64 uo = __shfl_sync(0xffffffffu, uoff, q), ro = __shfl_sync(0xffffffffu, roff, q);
-        const int lo = __shfl_sync(0xffffffffu, r_lo, q), hi = __shfl_sync(0xffffffffu, r_hi, q);
-        const double* Ucol = U + uo;
-        const int* rel = S.rel + ro;
-        for (int r = lo + lane; r < hi; r += 32) dstcol[rel[r]] += Ucol[r];
+      // Fixed child order; the FIRST 32-row chunk of entry q + 1 (its relative row and its value) is loaded before
+      // entry q is added: the adds of successive children may hit the same parent row and stay ordered, their loads
+      // need not wait for them (a band holds ~50 rows of a child, so the first chunk is usually the whole entry).
+      i64 uo = __shfl_sync(0xffffffffu, uoff, 0), ro = __shfl_sync(0xffffffffu, roff, 0);
+      int lo = __shfl_sync(0xffffffffu, r_lo, 0), hi = __shfl_sync(0xffffffffu, r_hi, 0);
+      int rel0 = 0;
+      double u0 = 0.0;
+      bool ok0 = lo + lane < hi;
+      if (ok0) {
+        rel0 = S.rel[ro + lo + lane];
+        u0 = U[uo + lo + lane];
+      }
+      for (int q = 0; q < cnt; ++q) {
+        const i64 uo_c = uo, ro_c = ro;
+        const int lo_c = lo, hi_c = hi, rel_c = rel0;
+        const double u_c = u0;
+        const bool ok_c = ok0;
+        if (q + 1 < cnt) {  // warp-uniform
+          uo = __shfl_sync(0xffffffffu, uoff, q + 1);
+          ro = __shfl_sync(0xffffffffu, roff, q + 1);
+          lo = __shfl_sync(0xffffffffu, r_lo, q + 1);
+          hi = __shfl_sync(0xffffffffu, r_hi, q + 1);
+          ok0 = lo + lane < hi;
+          if (ok0) {
+            rel0 = S.rel[ro + lo + lane];
+            u0 = U[uo + lo + lane];
+          }
+        }
+        if (ok_c) dstcol[rel_c] += u_c;
+        const double* Ucol = U + uo_c;
+        const int* rel = S.rel + ro_c;
+        for (int r = lo_c + 32 + lane; r < hi_c; r += 32) dstcol[rel[r]] += Ucol[r];
       }
     }
   } else {
