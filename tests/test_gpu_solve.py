@@ -330,3 +330,30 @@ def test_a_failed_step_leaves_the_last_good_iterate():
         assert res.status is SolveStatus.NUMERICAL_ERROR
     finally:
         dev.close()
+
+
+def test_bench_line_carries_the_contract_keys():
+    """bench.py on the smallest workload: one JSON line with the keys the driver and DESIGN section 7 rely on."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--workload", "C5_mpc", "--steps", "2", "--warmup",
+                          "1", "--e2e-steps", "1", "--batch-count", "24", "--cpu-budget", "5"], capture_output=True,
+                         text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "cpu_baseline", "clocks",
+                "ladder", "batch", "hot_path", "graphs"):
+        assert key in line, key
+    assert line["metric"] == "ipm_solve_seconds" and line["dtype"] == "f64" and line["higher_is_better"] is False
+    assert line["gpu_launches"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert set(line["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 1
+    rung = line["ladder"][0]
+    assert rung["cpu"]["source"].startswith("measured") and rung["iterations_equal"] and rung["objective_rel_diff"] < 1e-6
+    assert line["batch"]["instances"] == 24 and line["batch"]["not_solved"] == 0 and "lockstep" in line["batch"]["mode"]
+    assert line["graphs"]["direct_launch_sequences"] == 0
