@@ -1886,13 +1886,13 @@ qs_batch* qs_batch_create(int device, int64_t count) {
   bt->arena.slot_bytes = QS_BSTRIDE;
   bt->arena.slots = (int)count;
   const size_t total = (size_t)count * QS_BSTRIDE;
-  // the arena comes from the device's memory pool like every handle's memory (devmem.h): a second batch of the same
-  // size is pool bookkeeping, not a 16 GB driver mapping (measured 0.01 - 0.6 s, box and history dependent)
-  if (qs_dev_malloc((void**)&bt->arena.base, total) != cudaSuccess ||
+  // plain cudaMalloc: 10-50 ms for 16 GB.  (Taking the arena from the stream-ordered memory pool makes a SECOND batch
+  // of the same size free -- 3 ms -- but the first one pays the pool's growth: 0.6-0.9 s measured.)
+  if (cudaMalloc((void**)&bt->arena.base, total) != cudaSuccess ||
       cudaMallocHost((void**)&bt->sc_host, (size_t)count * SC_COUNT * sizeof(double)) != cudaSuccess ||
       cudaMallocHost((void**)&bt->flag_host, (size_t)count * sizeof(double)) != cudaSuccess) {
     g_error = std::string("qs_batch_create: ") + cudaGetErrorString(cudaGetLastError());
-    if (bt->arena.base) qs_dev_free(bt->arena.base);
+    if (bt->arena.base) cudaFree(bt->arena.base);
     if (bt->sc_host) cudaFreeHost(bt->sc_host);
     delete bt;
     return nullptr;
@@ -1928,8 +1928,7 @@ void qs_batch_destroy(qs_batch* bt) {
     v.erase(std::remove_if(v.begin(), v.end(), [&](const std::pair<char*, size_t>& a) { return a.first == bt->arena.base; }),
             v.end());
   }
-  cudaStreamSynchronize(nullptr);
-  qs_dev_free(bt->arena.base);  // after the arena left the registry: a real free (back to the pool)
+  cudaFree(bt->arena.base);
   cudaFreeHost(bt->sc_host);
   cudaFreeHost(bt->flag_host);
   delete bt;
