@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .errors import BadSparseStructure, NotInterior
-from .ipm import ORDERINGS, _objective
+from .ipm import ORDERINGS, _objective, _objective_pattern
 from .problem import ProblemData, Settings, SolveResult, SolveStatus, validate_problem
 
 _STATUS = {1: SolveStatus.SOLVED, 2: SolveStatus.MAX_ITERS, 3: SolveStatus.TIME_LIMIT, 4: SolveStatus.NUMERICAL_ERROR}
@@ -122,12 +122,13 @@ class BatchSolver:
         if bad:  # the reference lets NotInterior propagate (it is not a NumericalError, errors.py:32-37)
             raise NotInterior(f"instances {bad}: point is not strictly inside the cone")
         st = self.stats()
+        pat = _objective_pattern(d0.P)  # one pattern for the whole batch
         out = []
         for i in range(k):
             timers = {"batch_size": B, "batch_seconds": t2 - t1, "gpu_launches": st["gpu_launches"],
                       "host_syncs": st["host_syncs"]}
             out.append(SolveResult(status=_STATUS[int(status[i])], x=x[i].copy(), y=y[i].copy(), z=z[i].copy(),
-                                   s=s[i].copy(), objective=_objective(probs[i], x[i]), iterations=int(iters[i]),
+                                   s=s[i].copy(), objective=_objective(probs[i], x[i], pat), iterations=int(iters[i]),
                                    setup_seconds=(t1 - t0) / k, solve_seconds=(t2 - t1) / k,
                                    factor_count=int(iters[i]) + 1, solve_count=2 * int(iters[i]) + 2, timers=timers))
         return out

@@ -274,12 +274,17 @@ class DeviceSolver:
         return status, iterations, it
 
 
-def _objective(data: ProblemData, x: np.ndarray) -> float:
-    """0.5 x'Px + c'x from the upper-triangular P (ipm.py:296-297); O(nnz(P)) on the host, once."""
-    P = data.P
+def _objective_pattern(P):
+    """The pattern-only part of _objective (shared by every instance of a batch)."""
     cols = P.column_of_entry()
     rows = P.row_indices
-    w = np.where(rows == cols, 0.5, 1.0)
+    return rows, cols, np.where(rows == cols, 0.5, 1.0)
+
+
+def _objective(data: ProblemData, x: np.ndarray, pattern=None) -> float:
+    """0.5 x'Px + c'x from the upper-triangular P (ipm.py:296-297); O(nnz(P)) on the host, once."""
+    P = data.P
+    rows, cols, w = pattern if pattern is not None else _objective_pattern(P)
     return float(np.dot(w * P.values * x[rows], x[cols])) + float(np.dot(data.c, x))
 
 
