@@ -1242,6 +1242,11 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   std::string err = h->ls.analyze(N, an_p, an_i, h->knnz, h->d_Kp, h->d_Ki, (int)h->st.ordering,
                                   (const i64*)user_perm, nsoc, cstart.data(), csize.data(), n, h->st.static_reg, st);
   if (!err.empty()) return fail(h, err.find("memory") != std::string::npos ? QS_E_MEMORY : QS_E_INVALID, err);
+  if (h->direct_ok && nsoc > 0 && h->wp.kp_conic) {  // closed-form block positions hold: tiled K -> panel scatter
+    err = h->ls.set_cone_blocks((int)(n + p), (int)l, (int)nsoc, (const i64*)q, h->L.soc_ptr, h->wp.kp_conic,
+                                h->wp.cone_of_col, h->d_Kp, st);
+    if (!err.empty()) return fail(h, QS_E_MEMORY, err);
+  }
   h->tm.total[T_ANALYSIS] += h->ls.analysis_seconds;
   lap("ordering + symbolic + LDL' setup");
   h->have_problem = true;

@@ -78,6 +78,53 @@ __global__ void __launch_bounds__(LDL_THREADS) k_scatter_values(i64 nnz, const d
     L[amap[p]] = Kx[p];
 }
 
+// K columns without their SOC-block suffix (P, A', G' entries, orthant diagonal): a thread per K column
+__global__ void __launch_bounds__(LDL_THREADS) k_scatter_other(int N, ConeBlocks C, const double* __restrict__ Kx,
+                                                               const i64* __restrict__ amap, double* __restrict__ L) {
+  QS_BATCH(C, Kx, amap, L);
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < N; col += gridDim.x * blockDim.x) {
+    const i64 b = C.Kp[col];
+    i64 e = C.Kp[col + 1];
+    const int cc = col - C.n_p;  // conic index
+    if (cc >= C.l) {
+      const int k = C.cone_of_col[cc - C.l];
+      e -= (cc - C.soc_ptr[k]) + 1;  // the last j + 1 entries of the column are the block's
+    }
+    for (i64 p = b; p < e; ++p) L[amap[p]] = Kx[p];
+  }
+}
+
+// one 32 x 32 tile (ti <= tj) of a cone's packed upper triangle: read along the K columns, write along the panel
+// columns (whatever the map says: the transposition only makes the common case coalesced)
+__global__ void __launch_bounds__(256) k_scatter_blocks(ConeBlocks C, const double* __restrict__ Kx,
+                                                        const i64* __restrict__ amap, double* __restrict__ L) {
+  QS_BATCH(C, Kx, amap, L);
+  __shared__ double v[32][33];
+  __shared__ i64 a[32][33];
+  const int t = blockIdx.x;
+  const int k = C.tile_cone[t];
+  const int ti = C.tile_ij[2 * t], tj = C.tile_ij[2 * t + 1];
+  const int o = C.soc_ptr[k], q = C.soc_ptr[k + 1] - o;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int j = 32 * tj + jj, i = 32 * ti + tx;
+    i64 off = -1;
+    double val = 0.0;
+    if (j < q && i <= j) {
+      const i64 kpos = C.kp_conic[o + j] - (j + 1) + i;
+      val = Kx[kpos];
+      off = amap[kpos];
+    }
+    v[jj][tx] = val;
+    a[jj][tx] = off;
+  }
+  __syncthreads();
+  for (int ii = ty; ii < 32; ii += 8) {
+    const i64 off = a[tx][ii];  // entry (i = 32 ti + ii, j = 32 tj + tx): consecutive lanes, consecutive panel rows
+    if (off >= 0) L[off] = v[tx][ii];
+  }
+}
+
 __global__ void __launch_bounds__(LDL_THREADS) k_add_reg(int N, DevSym S, const double* reg, double* L) {
   QS_BATCH(S, reg, L);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
@@ -1754,6 +1801,32 @@ void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const voi
 }
 }  // namespace
 
+std::string LinSys::set_cone_blocks(int n_p, int l, int nsoc, const i64* q_host, const int* d_soc_ptr,
+                                    const i64* d_kp_conic, const int* d_cone_of_col, const i64* d_Kp, cudaStream_t st) {
+  have_cb = false;
+  if (nsoc <= 0) return "";
+  std::vector<int> tc;
+  std::vector<short> tij;
+  for (int k = 0; k < nsoc; ++k) {
+    const int T = (int)((q_host[k] + 31) / 32);
+    if (T > 32767) return "";  // a cone of more than 10^6 entries: keep the entry-by-entry scatter
+    for (int tj = 0; tj < T; ++tj)
+      for (int ti = 0; ti <= tj; ++ti) {
+        tc.push_back(k);
+        tij.push_back((short)ti);
+        tij.push_back((short)tj);
+      }
+  }
+  if (tc.size() >= ((size_t)1 << 31)) return "";
+  cb = ConeBlocks{n_p, l, nsoc, d_soc_ptr, d_kp_conic, d_cone_of_col, d_Kp, (int)tc.size(), nullptr, nullptr};
+  cb.tile_cone = upload(tc, &owned, &device_bytes, st);
+  cb.tile_ij = upload(tij, &owned, &device_bytes, st);
+  cudaStreamSynchronize(st);
+  if (!cb.tile_cone || !cb.tile_ij) return "cudaMalloc failed for the SOC block tile list";
+  have_cb = true;
+  return "";
+}
+
 void LinSys::factor(const double* d_Kx, double* scalars, cudaStream_t st) {
   run_graphed(factor_graphs, use_graphs, d_Kx, scalars, st, graph_counts, [&]() { factor_launches(d_Kx, scalars, st); });
 }
@@ -1765,7 +1838,13 @@ void LinSys::solve(const double* d_rhs, double* d_sol, cudaStream_t st) {
 void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t st) {
   qs_memset_b(L, 0, S.Loff[S.nsup] * 8, st);
   if (S.Uoff[S.nsup] > 0) qs_memset_b(U, 0, S.Uoff[S.nsup] * 8, st);
-  k_scatter_values<<<qs_grid(grid_for(knnz)), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
+  static const bool tiled_scatter = !(getenv("QS_LDL_TILED_SCATTER") && atoi(getenv("QS_LDL_TILED_SCATTER")) == 0);
+  if (have_cb && tiled_scatter) {
+    k_scatter_other<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, cb, d_Kx, amap, L);
+    k_scatter_blocks<<<qs_grid(cb.ntiles), 256, 0, st>>>(cb, d_Kx, amap, L);
+  } else {
+    k_scatter_values<<<qs_grid(grid_for(knnz)), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);
+  }
   k_add_reg<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, D, reg, L);
   auto leaf_grid = [&](int g) { return (unsigned)(((i64)n_leaf * g + LDL_THREADS - 1) / LDL_THREADS); };
   if (n_leaf > 0) QS_LEAF_DISPATCH(k_leaf_factor, leaf_grid, D, d_leaf, n_leaf, L, U, Dg, reg, dyn_eps, scalars)

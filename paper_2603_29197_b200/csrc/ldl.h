@@ -97,8 +97,32 @@ struct EaItem {
   int slot, band;
 };
 
+// Dense SOC blocks of K (upper triangles packed by columns) land TRANSPOSED in the panels of L: entry (i, j), i <= j,
+// of a cone goes to row j, column i of its front.  Scattering K entry by entry writes 8 bytes per 4 KB stride (each
+// store its own 32-byte sector).  With the block structure at hand the scatter runs tile by tile through shared
+// memory: read 32 x 32 along the K columns, write along the panel columns.
+struct ConeBlocks {
+  int n_p, l, nsoc;         // first conic K column, orthant size, cones
+  const int* soc_ptr;       // [nsoc+1] conic index of each cone's first row (starts at l)
+  const i64* kp_conic;      // [m] kp_conic[c] = K.col_pointers[n_p + c + 1]
+  const int* cone_of_col;   // [m - l]
+  const i64* Kp;            // K column pointers
+  int ntiles;
+  const int* tile_cone;     // [ntiles]
+  const short* tile_ij;     // [2 ntiles] (ti, tj), ti <= tj, of the cone's upper triangle
+  __device__ void shift(size_t off) {
+    qs_shift(off, soc_ptr), qs_shift(off, kp_conic), qs_shift(off, cone_of_col), qs_shift(off, Kp);
+    qs_shift(off, tile_cone), qs_shift(off, tile_ij);
+  }
+};
+
 struct LinSys {
   Symbolic S;
+  ConeBlocks cb{};
+  bool have_cb = false;
+  // after analyze(): the cone layout of the KKT matrix whose closed-form block positions were validated (capi.cu)
+  std::string set_cone_blocks(int n_p, int l, int nsoc, const i64* q_host, const int* d_soc_ptr, const i64* d_kp_conic,
+                              const int* d_cone_of_col, const i64* d_Kp, cudaStream_t st);
   DevSym D{};
   i64 N = 0, knnz = 0;
   // device storage
