@@ -1244,7 +1244,7 @@ int qs_setup(qs_handle* h, int64_t n, int64_t m, int64_t p, int64_t l, int64_t n
   if (!err.empty()) return fail(h, err.find("memory") != std::string::npos ? QS_E_MEMORY : QS_E_INVALID, err);
   if (h->direct_ok && nsoc > 0 && h->wp.kp_conic) {  // closed-form block positions hold: tiled K -> panel scatter
     err = h->ls.set_cone_blocks((int)(n + p), (int)l, (int)nsoc, (const i64*)q, h->L.soc_ptr, h->wp.kp_conic,
-                                h->wp.cone_of_col, h->d_Kp, st);
+                                h->wp.cone_of_col, h->d_Kp, h->Kp_h[n + p + l], st);
     if (!err.empty()) return fail(h, QS_E_MEMORY, err);
   }
   h->tm.total[T_ANALYSIS] += h->ls.analysis_seconds;

@@ -78,19 +78,20 @@ __global__ void __launch_bounds__(LDL_THREADS) k_scatter_values(i64 nnz, const d
     L[amap[p]] = Kx[p];
 }
 
-// K columns without their SOC-block suffix (P, A', G' entries, orthant diagonal): a thread per K column
+// The G' entries above the block in the SOC columns of K: a warp per column.  (Everything before the first SOC column
+// -- P, A', the orthant part -- holds no block and goes through k_scatter_values entry by entry: a K column there can be
+// one dense equality row, 10^5 entries in a budget constraint, which no per-column scheme should own.)
 __global__ void __launch_bounds__(LDL_THREADS) k_scatter_other(int N, ConeBlocks C, const double* __restrict__ Kx,
                                                                const i64* __restrict__ amap, double* __restrict__ L) {
   QS_BATCH(C, Kx, amap, L);
-  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < N; col += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 col = C.n_p + C.l + (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); col < N; col += nwarps) {
+    const int cc = (int)col - C.n_p;  // conic index, >= l
+    const int k = C.cone_of_col[cc - C.l];
     const i64 b = C.Kp[col];
-    i64 e = C.Kp[col + 1];
-    const int cc = col - C.n_p;  // conic index
-    if (cc >= C.l) {
-      const int k = C.cone_of_col[cc - C.l];
-      e -= (cc - C.soc_ptr[k]) + 1;  // the last j + 1 entries of the column are the block's
-    }
-    for (i64 p = b; p < e; ++p) L[amap[p]] = Kx[p];
+    const i64 e = C.Kp[col + 1] - ((cc - C.soc_ptr[k]) + 1);  // the last j + 1 entries of the column are the block's
+    for (i64 p = b + lane; p < e; p += 32) L[amap[p]] = Kx[p];
   }
 }
 
@@ -1802,7 +1803,8 @@ void run_graphed(std::vector<LinSys::GraphEntry>& cache, bool enabled, const voi
 }  // namespace
 
 std::string LinSys::set_cone_blocks(int n_p, int l, int nsoc, const i64* q_host, const int* d_soc_ptr,
-                                    const i64* d_kp_conic, const int* d_cone_of_col, const i64* d_Kp, cudaStream_t st) {
+                                    const i64* d_kp_conic, const int* d_cone_of_col, const i64* d_Kp, i64 flat_nnz,
+                                    cudaStream_t st) {
   have_cb = false;
   if (nsoc <= 0) return "";
   std::vector<int> tc;
@@ -1818,7 +1820,7 @@ std::string LinSys::set_cone_blocks(int n_p, int l, int nsoc, const i64* q_host,
       }
   }
   if (tc.size() >= ((size_t)1 << 31)) return "";
-  cb = ConeBlocks{n_p, l, nsoc, d_soc_ptr, d_kp_conic, d_cone_of_col, d_Kp, (int)tc.size(), nullptr, nullptr};
+  cb = ConeBlocks{n_p, l, nsoc, d_soc_ptr, d_kp_conic, d_cone_of_col, d_Kp, flat_nnz, (int)tc.size(), nullptr, nullptr};
   cb.tile_cone = upload(tc, &owned, &device_bytes, st);
   cb.tile_ij = upload(tij, &owned, &device_bytes, st);
   cudaStreamSynchronize(st);
@@ -1840,7 +1842,8 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
   if (S.Uoff[S.nsup] > 0) qs_memset_b(U, 0, S.Uoff[S.nsup] * 8, st);
   static const bool tiled_scatter = !(getenv("QS_LDL_TILED_SCATTER") && atoi(getenv("QS_LDL_TILED_SCATTER")) == 0);
   if (have_cb && tiled_scatter) {
-    k_scatter_other<<<qs_grid(grid_for(N)), LDL_THREADS, 0, st>>>((int)N, cb, d_Kx, amap, L);
+    if (cb.flat_nnz > 0) k_scatter_values<<<qs_grid(grid_for(cb.flat_nnz)), LDL_THREADS, 0, st>>>(cb.flat_nnz, d_Kx, amap, L);
+    k_scatter_other<<<qs_grid(grid_for((N - cb.n_p - cb.l) * 32)), LDL_THREADS, 0, st>>>((int)N, cb, d_Kx, amap, L);
     k_scatter_blocks<<<qs_grid(cb.ntiles), 256, 0, st>>>(cb, d_Kx, amap, L);
   } else {
     k_scatter_values<<<qs_grid(grid_for(knnz)), LDL_THREADS, 0, st>>>(knnz, d_Kx, amap, L);

@@ -107,6 +107,7 @@ struct ConeBlocks {
   const i64* kp_conic;      // [m] kp_conic[c] = K.col_pointers[n_p + c + 1]
   const int* cone_of_col;   // [m - l]
   const i64* Kp;            // K column pointers
+  i64 flat_nnz;             // K entries before the first SOC column: no block among them (scattered entry by entry)
   int ntiles;
   const int* tile_cone;     // [ntiles]
   const short* tile_ij;     // [2 ntiles] (ti, tj), ti <= tj, of the cone's upper triangle
@@ -122,7 +123,7 @@ struct LinSys {
   bool have_cb = false;
   // after analyze(): the cone layout of the KKT matrix whose closed-form block positions were validated (capi.cu)
   std::string set_cone_blocks(int n_p, int l, int nsoc, const i64* q_host, const int* d_soc_ptr, const i64* d_kp_conic,
-                              const int* d_cone_of_col, const i64* d_Kp, cudaStream_t st);
+                              const int* d_cone_of_col, const i64* d_Kp, i64 flat_nnz, cudaStream_t st);
   DevSym D{};
   i64 N = 0, knnz = 0;
   // device storage
