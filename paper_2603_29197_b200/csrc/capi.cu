@@ -37,6 +37,12 @@ struct DevMem {
   cudaStream_t stream[64] = {nullptr};
   std::unordered_set<void*> from_pool;  // pointers handed out by cudaMallocAsync
   std::vector<std::pair<char*, size_t>> arenas;  // live batch arenas (base, total bytes)
+  struct CachedArena {
+    int dev;
+    char* base;
+    size_t bytes;
+  };
+  std::vector<CachedArena> arena_cache;  // released arenas kept for the next batch (at most 2 per process)
 };
 DevMem g_devmem;
 }  // namespace
@@ -1734,6 +1740,7 @@ struct qs_batch {
   int device = 0;
   int B = 0;
   QsArena arena;
+  size_t arena_bytes = 0;       // allocated size (>= slots * stride when the arena was taken from the cache)
   qs_handle* h = nullptr;       // the handle of slot 0; every device pointer in it is valid in every slot + b * stride
   double* sc_host = nullptr;    // pinned [B][SC_COUNT]
   double* flag_host = nullptr;  // pinned [B]
@@ -1891,9 +1898,30 @@ qs_batch* qs_batch_create(int device, int64_t count) {
   bt->arena.slot_bytes = QS_BSTRIDE;
   bt->arena.slots = (int)count;
   const size_t total = (size_t)count * QS_BSTRIDE;
-  // plain cudaMalloc: 10-50 ms for 16 GB.  (Taking the arena from the stream-ordered memory pool makes a SECOND batch
-  // of the same size free -- 3 ms -- but the first one pays the pool's growth: 0.6-0.9 s measured.)
-  if (cudaMalloc((void**)&bt->arena.base, total) != cudaSuccess ||
+  // The arena: a released one of this device that is large enough (kept in a small cache by qs_batch_destroy, zeroed
+  // here: 2.5 ms for 16 GB), else plain cudaMalloc (10-50 ms for 16 GB, but now and then 0.5 s when the driver has to
+  // map again what a cudaFree just gave back -- every third bench run showed it).  The stream-ordered memory pool
+  // was tried for this: the second batch is free, the first pays 0.6-0.9 s of pool growth.
+  {
+    std::lock_guard<std::mutex> lk(g_devmem.mu);
+    int best = -1;
+    for (size_t k = 0; k < g_devmem.arena_cache.size(); ++k) {
+      const auto& c = g_devmem.arena_cache[k];
+      if (c.dev == device && c.bytes >= total && (best < 0 || c.bytes < g_devmem.arena_cache[best].bytes)) best = (int)k;
+    }
+    if (best >= 0) {
+      bt->arena.base = g_devmem.arena_cache[best].base;
+      bt->arena_bytes = g_devmem.arena_cache[best].bytes;
+      g_devmem.arena_cache.erase(g_devmem.arena_cache.begin() + best);
+    }
+  }
+  if (bt->arena.base) {
+    cudaMemset(bt->arena.base, 0, total);
+  } else {
+    bt->arena_bytes = total;
+    if (cudaMalloc((void**)&bt->arena.base, total) != cudaSuccess) bt->arena.base = nullptr;
+  }
+  if (!bt->arena.base ||
       cudaMallocHost((void**)&bt->sc_host, (size_t)count * SC_COUNT * sizeof(double)) != cudaSuccess ||
       cudaMallocHost((void**)&bt->flag_host, (size_t)count * sizeof(double)) != cudaSuccess) {
     g_error = std::string("qs_batch_create: ") + cudaGetErrorString(cudaGetLastError());
@@ -1933,7 +1961,18 @@ void qs_batch_destroy(qs_batch* bt) {
     v.erase(std::remove_if(v.begin(), v.end(), [&](const std::pair<char*, size_t>& a) { return a.first == bt->arena.base; }),
             v.end());
   }
-  cudaFree(bt->arena.base);
+  if (bt->arena.base) {
+    cudaDeviceSynchronize();  // nothing of this batch is in flight any more
+    bool kept = false;
+    {
+      std::lock_guard<std::mutex> lk(g_devmem.mu);
+      if (g_devmem.arena_cache.size() < 2) {
+        g_devmem.arena_cache.push_back(DevMem::CachedArena{bt->device, bt->arena.base, bt->arena_bytes});
+        kept = true;
+      }
+    }
+    if (!kept) cudaFree(bt->arena.base);
+  }
   cudaFreeHost(bt->sc_host);
   cudaFreeHost(bt->flag_host);
   delete bt;
