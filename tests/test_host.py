@@ -204,6 +204,16 @@ def test_api_surface_and_no_cpu_fallback():
     if _lib.load().qs_device_count() == 0:
         with pytest.raises(errors.CudaUnavailable):
             s.solve()
+        # the batched mode and the sharded batch driver fail as loudly: nothing solves on the CPU
+        from paper_2603_29197_b200 import configs
+        from paper_2603_29197_b200.batch import solve_shard
+        from paper_2603_29197_b200.batched import solve_batched
+
+        probs = [configs.make("C5_mpc", small=True, seed=i) for i in range(2)]
+        with pytest.raises(errors.CudaUnavailable):
+            solve_batched(probs)
+        with pytest.raises(errors.CudaUnavailable):
+            solve_shard(probs, device=0)
 
 
 def test_as_csc_accepts_dense_scipy_and_none():
