@@ -587,7 +587,21 @@ __global__ void __launch_bounds__(LDL_THREADS, 3)
     // left-looking panel step: block column [kb, kb+NB) (rows kb .. nr) receives the updates of ALL previous
     // pivot columns at once -- one pass with inner depth kb instead of kb/32 rank-32 passes over the panel
     if (kb >= f.ns) return;
-    if (left) {
+    if (left == 3) {
+      // wide left-looking step: TWO block columns [kb, kb + 2 NB) receive the updates of all previous pivots --
+      // the 64 x 64 tile is full (a 32-column step keeps half of the CTA's warps out of the multiply)
+      if (kb == 0) return;
+      k_lo = 0;
+      k_hi = kb;
+      c_lo = kb;
+      c_hi = min(f.ns, kb + 2 * NB);
+    } else if (left == 2) {
+      // second half of a wide step: pivots [kb, kb + NB) update the block column [kb + NB, kb + 2 NB) only
+      k_lo = kb;
+      k_hi = min(f.ns, kb + NB);
+      c_lo = k_hi;
+      c_hi = min(f.ns, kb + 2 * NB);
+    } else if (left) {
       if (kb == 0) return;
       k_lo = 0;
       k_hi = kb;
@@ -1900,8 +1914,18 @@ void LinSys::factor_launches(const double* d_Kx, double* scalars, cudaStream_t s
         k_front_blocked<1><<<qs_grid(nb_fronts), LDL_THREADS, 0, st>>>(D, lst, L, Dg, reg, dyn_eps, scalars);
       else if (fused)
         k_front_blocked<2><<<qs_grid(nb_fronts), LDL_THREADS, 0, st>>>(D, lst, L, Dg, reg, dyn_eps, scalars);
+      // left-looking levels advance two block columns per update launch (QS_LDL_WIDE=0: one)
+      static const bool wide = !(getenv("QS_LDL_WIDE") && atoi(getenv("QS_LDL_WIDE")) == 0);
       for (int kb = 0; kb < mx_ns && !fused; kb += NB) {
-        if (left && kb > 0) {  // bring block column kb up to date with the pivots [0, kb)
+        if (left && wide) {
+          const int nti = (mx_nr - kb + TS - 1) / TS;
+          dim3 gu(nti, nb_fronts);
+          if ((kb / NB) % 2 == 0) {
+            if (kb > 0) k_blk_update<false><<<qs_grid(gu), LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 3, L, U, Dg);
+          } else {  // the odd block column: only the pivots of the block column before it are missing
+            k_blk_update<false><<<qs_grid(gu), LDL_THREADS, 0, st>>>(D, lst, nullptr, kb - NB, 2, L, U, Dg);
+          }
+        } else if (left && kb > 0) {  // bring block column kb up to date with the pivots [0, kb)
           const int nti = (mx_nr - kb + TS - 1) / TS;
           dim3 gu(nti, nb_fronts);
           k_blk_update<false><<<qs_grid(gu), LDL_THREADS, 0, st>>>(D, lst, nullptr, kb, 1, L, U, Dg);
